@@ -1,0 +1,928 @@
+// api.cu -- the C ABI of include/gcp.h: argument validation, the context state
+// machine, and the host side of the hot path (which kernel runs when, with
+// which weights and counters).  All arithmetic runs in the kernels of
+// kernels.cuh; this file only orchestrates.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gcp_internal.h"
+
+using namespace gcp;
+
+namespace gcp {
+
+static thread_local std::string g_err;
+
+gcp_status set_error(gcp_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+gcp_status cuda_fail(gcp_ctx* c, cudaError_t e, const char* what) {
+    if (c) c->sticky = GCP_E_CUDA;
+    return set_error(GCP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+gcp_status nccl_fail(gcp_ctx* c, ncclResult_t r, const char* what) {
+    if (c) c->sticky = GCP_E_NCCL;
+    return set_error(GCP_E_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+static cudaEvent_t ev_get(gcp_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(gcp_ctx* c, int which, cudaEvent_t* ev) {
+    (void)which;
+    c->launches++;
+    *ev = nullptr;
+    if (!c->prof_on) return;
+    *ev = ev_get(c);
+    cudaEventRecord(*ev, c->stream);
+}
+
+void prof_end(gcp_ctx* c, int which, cudaEvent_t ev) {
+    if (!c->prof_on || !ev) return;
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->stream);
+    c->pending.push_back({ev, b, which});
+}
+
+static void prof_resolve(gcp_ctx* c) {
+    for (auto& p : c->pending) {
+        cudaEventSynchronize(p.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        c->prof_ms[p.which] += ms;
+        c->prof_n[p.which] += 1;
+        c->ev_pool.push_back(p.a);
+        c->ev_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
+}  // namespace gcp
+
+// ---------------------------------------------------------------- helpers
+namespace {
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+#define ENTER(c)                                                                     \
+    if (!(c)) return set_error(GCP_E_ARG, "null context");                          \
+    if ((c)->sticky != GCP_OK)                                                       \
+        return set_error(GCP_E_STATE, "context is in a sticky error state (" +      \
+                                          std::to_string((int)(c)->sticky) + ")");  \
+    DevGuard guard_((c)->dev)
+
+#define CUDA_TRY(c, x, what)                                   \
+    do {                                                       \
+        cudaError_t e_ = (x);                                  \
+        if (e_ != cudaSuccess) return cuda_fail((c), e_, what); \
+    } while (0)
+
+#define ST_TRY(x)                      \
+    do {                               \
+        gcp_status s_ = (x);           \
+        if (s_ != GCP_OK) return s_;   \
+    } while (0)
+
+int64_t alloc_count(int64_t total, int P, int w) { return total / P + (w < total % P ? 1 : 0); }
+
+double u128_to_double(unsigned __int128 v) { return (double)v; }
+
+double loss_lower(int loss) { return loss == GCP_LOSS_POISSON ? 0.0 : -INFINITY; }
+
+void free_model(gcp_ctx* c) {
+    void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C, &c->d_lambda, &c->d_Ack, &c->d_Bck, &c->d_Cck,
+                     &c->d_U,  &c->d_Bs, &c->d_Cs};
+    for (void** b : bufs) {
+        cudaFree(*b);
+        *b = nullptr;
+    }
+    c->have_model = false;
+    c->have_grad = false;
+    c->fit_active = false;
+}
+
+// Local sample counts for a GLOBAL total under the empty-strata rule
+// (SURVEY C4): a rank without nonzeros (zeros) draws none of that stratum.
+void local_counts(const gcp_ctx* c, int64_t s_nz, int64_t s_z, int64_t* p_w, int64_t* q_w) {
+    *p_w = c->N > 0 ? alloc_count(s_nz, c->P, c->rank) : 0;
+    *q_w = c->M > (unsigned __int128)c->N ? alloc_count(s_z, c->P, c->rank) : 0;
+}
+
+double weight_nz(const gcp_ctx* c, int64_t p_w) { return p_w > 0 ? (double)c->N / (double)p_w : 0.0; }
+double weight_z(const gcp_ctx* c, int64_t q_w) {
+    return q_w > 0 ? u128_to_double(c->M - (unsigned __int128)c->N) / (double)q_w : 0.0;
+}
+
+SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, uint32_t it, uint32_t kind_nz,
+                       uint32_t kind_z, int stratified) {
+    SampleArgs s;
+    s.rec = c->d_rec;
+    s.rec_words = c->rec_words;
+    s.val_words = c->val_words;
+    s.N = c->N;
+    s.hash = c->d_hash;
+    s.hash_mask = c->hash_slots - 1;
+    s.key128 = c->key128;
+    for (int k = 0; k < kMaxModes; ++k) s.bdim[k] = k < c->d ? (uint32_t)(c->hi[k] - c->lo[k]) : 1u;
+    s.p = p;
+    s.q = q;
+    s.seed = seed;
+    s.rank = (uint32_t)c->rank;
+    s.it = it;
+    s.kind_nz = kind_nz;
+    s.kind_z = kind_z;
+    s.stratified = stratified;
+    s.err_slot = c->d_err;
+    return s;
+}
+
+ModelArgs model_args(const gcp_ctx* c) {
+    ModelArgs m;
+    m.A = c->d_A;
+    m.G = c->d_G;
+    m.lambda = c->d_lambda;
+    for (int k = 0; k < kMaxModes; ++k) m.off[k] = k < c->d ? c->off[k] : 0;
+    m.R_pad = c->R_pad;
+    return m;
+}
+
+gcp_status ensure_partials(gcp_ctx* c, int n) {
+    if (n <= c->partials_cap) return GCP_OK;
+    cudaFree(c->d_partials);
+    c->d_partials = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->d_partials, sizeof(double) * (n + 1)), "partials");
+    c->partials_cap = n;
+    return GCP_OK;
+}
+
+// Check the rejection-cap flag after a synchronisation point.
+gcp_status check_err(gcp_ctx* c, const char* what) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream),
+             what);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
+    if (*c->h_err != ULLONG_MAX) {
+        c->sticky = GCP_E_REJECT_CAP;
+        return set_error(GCP_E_REJECT_CAP, std::string(what) + ": rank " + std::to_string(c->rank) +
+                                               " zero slot " + std::to_string(*c->h_err) +
+                                               " rejected 1000 times (reading R5)");
+    }
+    return GCP_OK;
+}
+
+// Run the sample kernel in loss mode over a stratified sample set and return the
+// local sum sum_s w f into *out_dev (device double).
+gcp_status run_loss_kernel(gcp_ctx* c, int loss, int64_t p, int64_t q, uint64_t seed, uint32_t it,
+                           uint32_t kind_nz, uint32_t kind_z, int stratified, int semi_nz, int prof_which,
+                           int loss_mode, double* out_dev) {
+    const int nb = c->grad_blocks;
+    ST_TRY(ensure_partials(c, nb));
+    const SampleArgs s = sample_args(c, p, q, seed, it, kind_nz, kind_z, stratified);
+    const ModelArgs m = model_args(c);
+    cudaEvent_t ev;
+    prof_begin(c, prof_which, &ev);
+    CUDA_TRY(c, launch_sample_kernel(c, s, m, loss, loss_mode, semi_nz, weight_nz(c, p), weight_z(c, q), 1,
+                                     c->d_partials, nb),
+             "sample kernel");
+    prof_end(c, prof_which, ev);
+    prof_begin(c, PROF_OTHER, &ev);
+    CUDA_TRY(c, launch_reduce_partials(c, c->d_partials, nb, out_dev), "reduce partials");
+    prof_end(c, PROF_OTHER, ev);
+    return GCP_OK;
+}
+
+size_t tsz(const gcp_ctx* c) { return c->prec == GCP_FP32 ? 4 : 8; }
+
+gcp_status checkpoint_save(gcp_ctx* c) {
+    const size_t bytes = (size_t)c->n_coef * tsz(c);
+    if (!c->d_Ack) {
+        CUDA_TRY(c, cudaMalloc(&c->d_Ack, bytes), "checkpoint alloc");
+        CUDA_TRY(c, cudaMalloc(&c->d_Bck, bytes), "checkpoint alloc");
+        CUDA_TRY(c, cudaMalloc(&c->d_Cck, bytes), "checkpoint alloc");
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_Ack, c->d_A, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_Bck, c->d_B, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_Cck, c->d_C, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
+    c->t_ck = c->t;
+    c->ts_ck = c->ts;
+    return GCP_OK;
+}
+
+gcp_status checkpoint_restore(gcp_ctx* c) {
+    const size_t bytes = (size_t)c->n_coef * tsz(c);
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_A, c->d_Ack, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_B, c->d_Bck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_C, c->d_Cck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
+    CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "restore");
+    c->t = c->t_ck;
+    c->ts = c->ts_ck;
+    return GCP_OK;
+}
+
+// FedAdam server copy U <- current model, server moments zeroed (start of a fit).
+gcp_status server_reset(gcp_ctx* c) {
+    if (c->mode != GCP_DIST_ASYNC_FEDADAM) return GCP_OK;
+    const size_t bytes = (size_t)c->n_coef * tsz(c);
+    if (!c->d_U) {
+        CUDA_TRY(c, cudaMalloc(&c->d_U, bytes), "server alloc");
+        CUDA_TRY(c, cudaMalloc(&c->d_Bs, bytes), "server alloc");
+        CUDA_TRY(c, cudaMalloc(&c->d_Cs, bytes), "server alloc");
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_U, c->d_A, bytes, cudaMemcpyDeviceToDevice, c->stream), "server reset");
+    CUDA_TRY(c, cudaMemsetAsync(c->d_Bs, 0, bytes, c->stream), "server reset");
+    CUDA_TRY(c, cudaMemsetAsync(c->d_Cs, 0, bytes, c->stream), "server reset");
+    c->ts = 0;
+    return GCP_OK;
+}
+
+bool valid_loss(int loss) { return loss >= 0 && loss <= 2; }
+
+}  // namespace
+
+// ================================================================ ABI
+extern "C" {
+
+const char* gcp_last_error(void) { return g_err.c_str(); }
+
+gcp_status gcp_create(gcp_ctx** out, int cuda_device, void* cuda_stream, gcp_precision prec) {
+    if (!out) return set_error(GCP_E_ARG, "gcp_create: out is NULL");
+    *out = nullptr;
+    if (prec != GCP_FP32 && prec != GCP_FP64) return set_error(GCP_E_ARG, "gcp_create: bad precision");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return set_error(GCP_E_CUDA, "gcp_create: no CUDA device");
+    if (cuda_device < 0 || cuda_device >= ndev) return set_error(GCP_E_ARG, "gcp_create: bad device");
+    DevGuard g(cuda_device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess)
+        return set_error(GCP_E_CUDA, "gcp_create: cudaGetDeviceProperties failed");
+    if (prop.major != 10) return set_error(GCP_E_CUDA, "gcp_create: libgcp is built for sm_100a (B200) only");
+    gcp_ctx* c = new gcp_ctx();
+    c->dev = cuda_device;
+    c->stream = (cudaStream_t)cuda_stream;
+    c->prec = prec;
+    c->tsize = prec == GCP_FP32 ? 4 : 8;
+    c->sm_count = prop.multiProcessorCount;
+    if (cudaMallocHost(&c->h_scalar, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess ||
+        cudaMalloc(&c->d_err, 64) != cudaSuccess) {
+        gcp_destroy(c);
+        return set_error(GCP_E_OOM, "gcp_create: allocation failed");
+    }
+    cudaMemsetAsync(c->d_err, 0xFF, sizeof(unsigned long long), c->stream);
+    cudaStreamSynchronize(c->stream);
+    *out = c;
+    return GCP_OK;
+}
+
+void gcp_destroy(gcp_ctx* c) {
+    if (!c) return;
+    DevGuard g(c->dev);
+    cudaStreamSynchronize(c->stream);
+    free_model(c);
+    cudaFree(c->d_rec);
+    cudaFree(c->d_hash);
+    cudaFree(c->d_partials);
+    cudaFree(c->d_err);
+    if (c->h_scalar) cudaFreeHost(c->h_scalar);
+    if (c->h_err) cudaFreeHost(c->h_err);
+    for (auto& p : c->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (int k = 0; k < kMaxModes; ++k)
+        if (c->slice[k]) ncclCommDestroy(c->slice[k]);
+    if (c->world) ncclCommDestroy(c->world);
+    delete c;
+}
+
+gcp_status gcp_dist_set_async(gcp_ctx* c, int64_t tau, const gcp_adam_params* server) {
+    ENTER(c);
+    if (tau < 0) return set_error(GCP_E_ARG, "gcp_dist_set_async: tau < 0");
+    c->tau = tau;
+    if (server) {
+        c->server = *server;
+        c->server_set = true;
+    }
+    return GCP_OK;
+}
+
+gcp_status gcp_tensor_create(gcp_ctx* c, int d, const int64_t* dims, int64_t nnz, const int64_t* subs,
+                             const double* vals) {
+    ENTER(c);
+    if (d < 2 || d > kMaxD) return set_error(GCP_E_ARG, "gcp_tensor_create: need 2 <= d <= 6");
+    if (!dims || nnz < 0 || (nnz > 0 && (!subs || !vals)))
+        return set_error(GCP_E_ARG, "gcp_tensor_create: bad pointers / nnz");
+    for (int k = 0; k < d; ++k)
+        if (dims[k] < 1 || dims[k] > 0xFFFFFFFFLL)
+            return set_error(GCP_E_ARG, "gcp_tensor_create: each I_k must be in [1, 2^32-1]");
+    if (c->P > 1 && !c->dist_ready) return set_error(GCP_E_STATE, "gcp_tensor_create: gcp_dist_init first");
+    // stage the geometry
+    gcp_ctx* g = new gcp_ctx();
+    g->d = d;
+    int grid[kMaxModes];
+    if (c->P > 1) {
+        if (c->grid_given) {
+            int64_t prod = 1;
+            for (int k = 0; k < d; ++k) prod *= c->grid[k];
+            if (prod != c->P) {
+                delete g;
+                return set_error(GCP_E_ARG, "gcp_tensor_create: grid product != nranks");
+            }
+            for (int k = 0; k < d; ++k) grid[k] = c->grid[k];
+        } else {
+            gcp_status s = gcp_grid_plan(c->P, d, dims, grid, nullptr, nullptr);
+            if (s != GCP_OK) { delete g; return s; }
+        }
+    } else {
+        for (int k = 0; k < d; ++k) grid[k] = 1;
+    }
+    {
+        // rank coordinates (row-major, b_1 slowest) and ceil-based block bounds (reading R14)
+        int rem = c->rank;
+        int b[kMaxModes];
+        for (int k = d - 1; k >= 0; --k) {
+            b[k] = rem % grid[k];
+            rem /= grid[k];
+        }
+        g->M = 1;
+        for (int k = 0; k < d; ++k) {
+            const int64_t ck = (dims[k] + grid[k] - 1) / grid[k];
+            g->dims[k] = dims[k];
+            g->lo[k] = std::min<int64_t>(b[k] * ck, dims[k]);
+            g->hi[k] = std::min<int64_t>((b[k] + 1) * ck, dims[k]);
+            g->M *= (unsigned __int128)(g->hi[k] - g->lo[k]);
+        }
+    }
+    gcp_status st = ingest(c, g, nnz, subs, vals);
+    if (st != GCP_OK) {
+        delete g;
+        return st;
+    }
+    free_model(c);
+    c->d = d;
+    for (int k = 0; k < kMaxModes; ++k) {
+        c->dims[k] = k < d ? g->dims[k] : 0;
+        c->lo[k] = k < d ? g->lo[k] : 0;
+        c->hi[k] = k < d ? g->hi[k] : 0;
+        c->grid[k] = k < d ? grid[k] : 0;
+    }
+    c->M = g->M;
+    c->N = nnz;
+    delete g;
+    c->bound = false;
+    // global N and "some rank has zeros"
+    int64_t agg[2] = {nnz, c->M > (unsigned __int128)nnz ? 1 : 0};
+    if (c->P > 1) {
+        ST_TRY(dist_make_slices(c));
+        ST_TRY(dist_allreduce_i64_host(c, agg, 2));
+    } else {
+        for (int k = 0; k < kMaxModes; ++k) {
+            c->slice_size[k] = 1;
+            c->slice_rank[k] = 0;
+        }
+    }
+    c->N_global = agg[0];
+    c->any_zero_global = agg[1] > 0;
+    c->have_tensor = true;
+    return GCP_OK;
+}
+
+gcp_status gcp_tensor_info(gcp_ctx* c, int64_t* nnz_local, int64_t* lo, int64_t* hi, double* M_local,
+                           int64_t* nnz_global) {
+    ENTER(c);
+    if (!c->have_tensor) return set_error(GCP_E_STATE, "no tensor");
+    if (nnz_local) *nnz_local = c->N;
+    for (int k = 0; k < c->d; ++k) {
+        if (lo) lo[k] = c->lo[k];
+        if (hi) hi[k] = c->hi[k];
+    }
+    if (M_local) *M_local = u128_to_double(c->M);
+    if (nnz_global) *nnz_global = c->N_global;
+    return GCP_OK;
+}
+
+gcp_status gcp_tensor_export_sorted(gcp_ctx* c, int64_t first, int64_t count, int64_t* subs_out,
+                                    double* vals_out) {
+    ENTER(c);
+    if (!c->have_tensor) return set_error(GCP_E_STATE, "no tensor");
+    if (first < 0 || count < 0 || first + count > c->N) return set_error(GCP_E_RANGE, "export_sorted: range");
+    if (count == 0) return GCP_OK;
+    std::vector<uint32_t> rec((size_t)count * c->rec_words);
+    CUDA_TRY(c, cudaMemcpyAsync(rec.data(), c->d_rec + first * c->rec_words, rec.size() * 4,
+                                cudaMemcpyDeviceToHost, c->stream),
+             "export_sorted");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), "export_sorted");
+    for (int64_t n = 0; n < count; ++n) {
+        const uint32_t* r = &rec[(size_t)n * c->rec_words];
+        if (vals_out) {
+            if (c->val_words == 1) {
+                float f;
+                memcpy(&f, r, 4);
+                vals_out[n] = f;
+            } else {
+                memcpy(&vals_out[n], r, 8);
+            }
+        }
+        if (subs_out)
+            for (int k = 0; k < c->d; ++k) subs_out[n * c->d + k] = c->lo[k] + (int64_t)r[c->val_words + k];
+    }
+    return GCP_OK;
+}
+
+gcp_status gcp_tensor_contains(gcp_ctx* c, int64_t n, const int64_t* coords, int8_t* out) {
+    ENTER(c);
+    if (!c->have_tensor) return set_error(GCP_E_STATE, "no tensor");
+    if (n < 0 || (n > 0 && (!coords || !out))) return set_error(GCP_E_ARG, "contains: args");
+    for (int64_t x = 0; x < n; ++x)
+        for (int k = 0; k < c->d; ++k)
+            if (coords[x * c->d + k] < c->lo[k] || coords[x * c->d + k] >= c->hi[k])
+                return set_error(GCP_E_RANGE, "contains: coordinate outside block");
+    if (n == 0) return GCP_OK;
+    int64_t* dc = nullptr;
+    int8_t* dout = nullptr;
+    CUDA_TRY(c, cudaMalloc(&dc, sizeof(int64_t) * n * c->d), "contains");
+    CUDA_TRY(c, cudaMalloc(&dout, n), "contains");
+    CUDA_TRY(c, cudaMemcpyAsync(dc, coords, sizeof(int64_t) * n * c->d, cudaMemcpyHostToDevice, c->stream), "contains");
+    cudaEvent_t ev;
+    prof_begin(c, PROF_OTHER, &ev);
+    CUDA_TRY(c, launch_contains(c, n, dc, dout), "contains");
+    prof_end(c, PROF_OTHER, ev);
+    CUDA_TRY(c, cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, c->stream), "contains");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), "contains");
+    cudaFree(dc);
+    cudaFree(dout);
+    return GCP_OK;
+}
+
+gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
+    ENTER(c);
+    if (!c->have_tensor) return set_error(GCP_E_STATE, "gcp_model_init: no tensor");
+    const int rmax = c->prec == GCP_FP32 ? 128 : 64;
+    if (R < 1 || R > rmax) return set_error(GCP_E_ARG, "gcp_model_init: need 1 <= R <= 128 (fp32) / 64 (fp64)");
+    free_model(c);
+    c->R = R;
+    c->R_pad = (R + 3) / 4 * 4;
+    int64_t off = 0;
+    for (int k = 0; k < c->d; ++k) {
+        const int64_t b = c->hi[k] - c->lo[k];
+        const int64_t g = (c->P > 1 && c->mode == GCP_DIST_SYNC) ? c->slice_size[k] : 1;
+        c->rows[k] = (b + g - 1) / g * g;
+        c->off[k] = off;
+        off += c->rows[k] * c->R_pad;
+    }
+    c->n_coef = off;
+    const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
+    void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C};
+    for (void** b : bufs) {
+        cudaError_t e = cudaMalloc(b, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            free_model(c);
+            return set_error(GCP_E_OOM, "gcp_model_init: out of device memory");
+        }
+    }
+    CUDA_TRY(c, cudaMalloc(&c->d_lambda, (size_t)c->R_pad * tsz(c)), "model lambda");
+    CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "model init");
+    CUDA_TRY(c, cudaMemsetAsync(c->d_B, 0, bytes, c->stream), "model init");
+    CUDA_TRY(c, cudaMemsetAsync(c->d_C, 0, bytes, c->stream), "model init");
+    {
+        std::vector<double> lam64(c->R_pad, 0.0);
+        std::vector<float> lam32(c->R_pad, 0.0f);
+        for (int r = 0; r < R; ++r) lam64[r] = lam32[r] = 1.0;
+        const void* src = c->prec == GCP_FP32 ? (const void*)lam32.data() : (const void*)lam64.data();
+        CUDA_TRY(c, cudaMemcpyAsync(c->d_lambda, src, (size_t)c->R_pad * tsz(c), cudaMemcpyHostToDevice, c->stream),
+                 "lambda");
+        int64_t goff[kMaxModes] = {0};
+        int64_t acc = 0;
+        for (int k = 0; k < c->d; ++k) {
+            goff[k] = acc;
+            acc += c->dims[k] * R;
+        }
+        cudaEvent_t ev;
+        prof_begin(c, PROF_OTHER, &ev);
+        CUDA_TRY(c, launch_init(c, seed, goff), "factor init");
+        prof_end(c, PROF_OTHER, ev);
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model init");
+    }
+    c->t = 0;
+    c->ts = 0;
+    c->it = 0;
+    c->grad_blocks = sample_kernel_blocks(c);
+    ST_TRY(ensure_partials(c, c->grad_blocks));
+    c->have_model = true;
+    c->have_grad = false;
+    return GCP_OK;
+}
+
+gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* lambda) {
+    ENTER(c);
+    if (!c->have_model) return set_error(GCP_E_STATE, "gcp_model_set: no model");
+    if (k < 0 || k >= c->d) return set_error(GCP_E_RANGE, "gcp_model_set: mode out of range");
+    if (!rows) return set_error(GCP_E_ARG, "gcp_model_set: rows NULL");
+    const int64_t b = c->hi[k] - c->lo[k];
+    const size_t n = (size_t)b * c->R_pad;
+    if (c->prec == GCP_FP32) {
+        std::vector<float> h(n, 0.f);
+        for (int64_t i = 0; i < b; ++i)
+            for (int r = 0; r < c->R; ++r) h[(size_t)i * c->R_pad + r] = (float)rows[i * c->R + r];
+        CUDA_TRY(c, cudaMemcpyAsync((float*)c->d_A + c->off[k], h.data(), n * 4, cudaMemcpyHostToDevice, c->stream),
+                 "model_set");
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
+    } else {
+        std::vector<double> h(n, 0.0);
+        for (int64_t i = 0; i < b; ++i)
+            for (int r = 0; r < c->R; ++r) h[(size_t)i * c->R_pad + r] = rows[i * c->R + r];
+        CUDA_TRY(c, cudaMemcpyAsync((double*)c->d_A + c->off[k], h.data(), n * 8, cudaMemcpyHostToDevice, c->stream),
+                 "model_set");
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
+    }
+    if (lambda) {
+        std::vector<double> l64(c->R_pad, 0.0);
+        std::vector<float> l32(c->R_pad, 0.f);
+        for (int r = 0; r < c->R; ++r) {
+            l64[r] = lambda[r];
+            l32[r] = (float)lambda[r];
+        }
+        const void* src = c->prec == GCP_FP32 ? (const void*)l32.data() : (const void*)l64.data();
+        CUDA_TRY(c, cudaMemcpyAsync(c->d_lambda, src, (size_t)c->R_pad * tsz(c), cudaMemcpyHostToDevice, c->stream),
+                 "model_set lambda");
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
+    }
+    return GCP_OK;
+}
+
+static gcp_status read_rows(gcp_ctx* c, const void* base, int k, double* out, const char* what) {
+    const int64_t b = c->hi[k] - c->lo[k];
+    const size_t n = (size_t)b * c->R_pad;
+    if (c->prec == GCP_FP32) {
+        std::vector<float> h(n);
+        CUDA_TRY(c, cudaMemcpyAsync(h.data(), (const float*)base + c->off[k], n * 4, cudaMemcpyDeviceToHost, c->stream),
+                 what);
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
+        for (int64_t i = 0; i < b; ++i)
+            for (int r = 0; r < c->R; ++r) out[i * c->R + r] = h[(size_t)i * c->R_pad + r];
+    } else {
+        std::vector<double> h(n);
+        CUDA_TRY(c, cudaMemcpyAsync(h.data(), (const double*)base + c->off[k], n * 8, cudaMemcpyDeviceToHost,
+                                    c->stream),
+                 what);
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
+        for (int64_t i = 0; i < b; ++i)
+            for (int r = 0; r < c->R; ++r) out[i * c->R + r] = h[(size_t)i * c->R_pad + r];
+    }
+    return GCP_OK;
+}
+
+gcp_status gcp_model_get(gcp_ctx* c, int k, double* rows_out) {
+    ENTER(c);
+    if (!c->have_model) return set_error(GCP_E_STATE, "gcp_model_get: no model");
+    if (k < 0 || k >= c->d) return set_error(GCP_E_RANGE, "gcp_model_get: mode out of range");
+    if (!rows_out) return set_error(GCP_E_ARG, "gcp_model_get: NULL");
+    return read_rows(c, c->d_A, k, rows_out, "model_get");
+}
+
+gcp_status gcp_grad_get(gcp_ctx* c, int k, double* out) {
+    ENTER(c);
+    if (!c->have_model) return set_error(GCP_E_STATE, "gcp_grad_get: no model");
+    if (k < 0 || k >= c->d) return set_error(GCP_E_RANGE, "gcp_grad_get: mode out of range");
+    if (!out) return set_error(GCP_E_ARG, "gcp_grad_get: NULL");
+    ST_TRY(check_err(c, "gcp_grad_get"));
+    return read_rows(c, c->d_G, k, out, "grad_get");
+}
+
+gcp_status gcp_sample(gcp_ctx* c, gcp_strategy strategy, int64_t s_nz, int64_t s_z, uint64_t seed) {
+    ENTER(c);
+    if (!c->have_tensor) return set_error(GCP_E_STATE, "gcp_sample: no tensor");
+    if (strategy != GCP_STRATIFIED && strategy != GCP_SEMI_STRATIFIED)
+        return set_error(GCP_E_ARG, "gcp_sample: bad strategy");
+    if (s_nz < 0 || s_z < 0 || s_nz + s_z == 0) return set_error(GCP_E_ARG, "gcp_sample: need p, q >= 0, p + q > 0");
+    if (s_nz > 0 && c->N_global == 0) return set_error(GCP_E_NO_NONZEROS, "gcp_sample: tensor has no nonzeros");
+    if (s_z > 0 && strategy == GCP_STRATIFIED && !c->any_zero_global)
+        return set_error(GCP_E_NO_ZEROS, "gcp_sample: tensor has no zeros");
+    int64_t p_w, q_w;
+    local_counts(c, s_nz, s_z, &p_w, &q_w);
+    if (p_w >= (int64_t)1 << 32 || q_w >= (int64_t)1 << 32)
+        return set_error(GCP_E_ARG, "gcp_sample: >= 2^32 slots per rank");
+    c->strategy = strategy;
+    c->s_nz = s_nz;
+    c->s_z = s_z;
+    c->p_w = p_w;
+    c->q_w = q_w;
+    c->seed = seed;
+    c->bound = true;
+    return GCP_OK;
+}
+
+gcp_status gcp_sample_export(gcp_ctx* c, int stratum, int64_t first, int64_t count, int64_t* subs_out,
+                             int64_t* j_out, double* w_out, int32_t* attempts_out) {
+    ENTER(c);
+    if (!c->bound) return set_error(GCP_E_STATE, "gcp_sample_export: call gcp_sample first");
+    if (stratum != 0 && stratum != 1) return set_error(GCP_E_ARG, "gcp_sample_export: stratum must be 0 or 1");
+    const int64_t n = stratum == 0 ? c->p_w : c->q_w;
+    if (first < 0 || count < 0 || first + count > n) return set_error(GCP_E_RANGE, "gcp_sample_export: slot range");
+    if (!subs_out) return set_error(GCP_E_ARG, "gcp_sample_export: subs_out NULL");
+    if (count == 0) return GCP_OK;
+    const int stratified = c->strategy == GCP_STRATIFIED;
+    const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
+    int64_t *d_subs = nullptr, *d_j = nullptr, *d_lo = nullptr;
+    int32_t* d_att = nullptr;
+    CUDA_TRY(c, cudaMalloc(&d_subs, sizeof(int64_t) * count * c->d), "export");
+    CUDA_TRY(c, cudaMalloc(&d_j, sizeof(int64_t) * count), "export");
+    CUDA_TRY(c, cudaMalloc(&d_att, sizeof(int32_t) * count), "export");
+    CUDA_TRY(c, cudaMalloc(&d_lo, sizeof(int64_t) * kMaxModes), "export");
+    CUDA_TRY(c, cudaMemcpyAsync(d_lo, c->lo, sizeof(int64_t) * kMaxModes, cudaMemcpyHostToDevice, c->stream), "export");
+    cudaEvent_t ev;
+    prof_begin(c, PROF_OTHER, &ev);
+    CUDA_TRY(c, launch_export(c, s, stratum, (stratum == 0 ? 0 : c->p_w) + first, count, d_lo, d_subs, d_j, d_att),
+             "export");
+    prof_end(c, PROF_OTHER, ev);
+    CUDA_TRY(c, cudaMemcpyAsync(subs_out, d_subs, sizeof(int64_t) * count * c->d, cudaMemcpyDeviceToHost, c->stream),
+             "export");
+    if (j_out) CUDA_TRY(c, cudaMemcpyAsync(j_out, d_j, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c->stream), "export");
+    if (attempts_out)
+        CUDA_TRY(c, cudaMemcpyAsync(attempts_out, d_att, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream),
+                 "export");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), "export");
+    cudaFree(d_subs);
+    cudaFree(d_j);
+    cudaFree(d_att);
+    cudaFree(d_lo);
+    if (w_out) {
+        const double w = stratum == 0 ? weight_nz(c, c->p_w) : weight_z(c, c->q_w);
+        for (int64_t i = 0; i < count; ++i) w_out[i] = w;
+    }
+    return check_err(c, "gcp_sample_export");
+}
+
+gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
+    ENTER(c);
+    if (!c->have_model || !c->bound) return set_error(GCP_E_STATE, "gcp_loss_grad: need model and gcp_sample");
+    if (!valid_loss(loss)) return set_error(GCP_E_ARG, "gcp_loss_grad: bad loss");
+    // async schemes: averaging / server step before this iteration's sampling (Alg. 3-4)
+    if (c->mode != GCP_DIST_SYNC && c->tau > 0 && ((int64_t)c->it + 1) % c->tau == 0 && !c->have_grad)
+        ST_TRY(dist_async_sync(c));
+    c->last_loss = loss;
+    const int stratified = c->strategy == GCP_STRATIFIED;
+    const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
+    const ModelArgs m = model_args(c);
+    const int with_loss = sampled_loss_out != nullptr;
+    cudaEvent_t ev;
+    prof_begin(c, PROF_GRAD, &ev);
+    CUDA_TRY(c, launch_sample_kernel(c, s, m, loss, 0, !stratified, weight_nz(c, c->p_w), weight_z(c, c->q_w),
+                                     with_loss, c->d_partials, c->grad_blocks),
+             "gcp_loss_grad");
+    prof_end(c, PROF_GRAD, ev);
+    c->have_grad = true;
+    if (with_loss) {
+        prof_begin(c, PROF_OTHER, &ev);
+        CUDA_TRY(c, launch_reduce_partials(c, c->d_partials, c->grad_blocks, (double*)c->d_partials + c->partials_cap),
+                 "reduce");
+        prof_end(c, PROF_OTHER, ev);
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_scalar, (double*)c->d_partials + c->partials_cap, 8, cudaMemcpyDeviceToHost,
+                                    c->stream),
+                 "gcp_loss_grad");
+        ST_TRY(check_err(c, "gcp_loss_grad"));
+        *sampled_loss_out = *c->h_scalar;
+    }
+    return GCP_OK;
+}
+
+gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
+    ENTER(c);
+    if (!p) return set_error(GCP_E_ARG, "gcp_adam_step: NULL params");
+    if (!c->have_grad) return set_error(GCP_E_STATE, "gcp_adam_step: no gradient (call gcp_loss_grad)");
+    if (!(p->beta1 >= 0 && p->beta1 < 1 && p->beta2 >= 0 && p->beta2 < 1 && p->eps > 0 && p->rate >= 0))
+        return set_error(GCP_E_ARG, "gcp_adam_step: need 0 <= beta < 1, eps > 0, rate >= 0");
+    const double lower = std::isnan(p->lower) ? loss_lower(c->last_loss) : p->lower;
+    c->t += 1;
+    Segment seg;
+    seg.n = 0;
+    const bool sharded = c->P > 1 && c->mode == GCP_DIST_SYNC;
+    if (sharded) {
+        ST_TRY(dist_sync_exchange_pre(c));
+        for (int k = 0; k < c->d; ++k) {
+            const int64_t shard = c->rows[k] / c->slice_size[k];
+            seg.start[seg.n] = c->off[k] + (int64_t)c->slice_rank[k] * shard * c->R_pad;
+            seg.len[seg.n] = shard * c->R_pad;
+            seg.n++;
+        }
+    } else {
+        seg.start[0] = 0;
+        seg.len[0] = c->n_coef;
+        seg.n = 1;
+    }
+    cudaEvent_t ev;
+    prof_begin(c, PROF_ADAM, &ev);
+    CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower, c->t,
+                            sharded ? 0 : 1),
+             "gcp_adam_step");
+    prof_end(c, PROF_ADAM, ev);
+    if (sharded) {
+        CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, (size_t)c->n_coef * tsz(c), c->stream), "adam G reset");
+        ST_TRY(dist_sync_exchange_post(c));
+    }
+    c->it += 1;
+    c->have_grad = false;
+    return GCP_OK;
+}
+
+gcp_status gcp_loss_estimate(gcp_ctx* c, gcp_loss loss, int64_t f_nz, int64_t f_z, uint64_t seed, double* out) {
+    ENTER(c);
+    if (!c->have_model) return set_error(GCP_E_STATE, "gcp_loss_estimate: no model");
+    if (!valid_loss(loss)) return set_error(GCP_E_ARG, "gcp_loss_estimate: bad loss");
+    if (!out || f_nz < 0 || f_z < 0 || f_nz + f_z == 0) return set_error(GCP_E_ARG, "gcp_loss_estimate: args");
+    if (f_nz > 0 && c->N_global == 0) return set_error(GCP_E_NO_NONZEROS, "gcp_loss_estimate: no nonzeros");
+    if (f_z > 0 && !c->any_zero_global) return set_error(GCP_E_NO_ZEROS, "gcp_loss_estimate: no zeros");
+    int64_t p, q;
+    local_counts(c, f_nz, f_z, &p, &q);
+    double* dout = (double*)c->d_partials + c->partials_cap;
+    ST_TRY(run_loss_kernel(c, loss, p, q, seed, 0xFFFFFFFFu, KIND_F_NZ, KIND_F_Z, 1, 0, PROF_LOSS, 1, dout));
+    if (c->P > 1) ST_TRY(dist_allreduce_scalar(c, dout));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_scalar, dout, 8, cudaMemcpyDeviceToHost, c->stream), "loss_estimate");
+    ST_TRY(check_err(c, "gcp_loss_estimate"));
+    *out = *c->h_scalar;
+    return GCP_OK;
+}
+
+gcp_status gcp_fit_begin(gcp_ctx* c, const gcp_fit_params* p, double* initial_est) {
+    ENTER(c);
+    if (!p) return set_error(GCP_E_ARG, "gcp_fit_begin: NULL params");
+    if (!c->have_model) return set_error(GCP_E_STATE, "gcp_fit_begin: no model");
+    if (p->epochs < 0 || p->iters_per_epoch < 1 || p->max_fails < 1 || !(p->decay >= 0) || !valid_loss(p->loss))
+        return set_error(GCP_E_ARG, "gcp_fit_begin: bad epoch parameters");
+    if (c->mode != GCP_DIST_SYNC && p->tau < 1) return set_error(GCP_E_ARG, "gcp_fit_begin: async needs tau >= 1");
+    ST_TRY(gcp_sample(c, p->strategy, p->s_nz, p->s_z, p->seed));
+    c->fp = *p;
+    c->rate = p->adam.rate;
+    c->fails = 0;
+    c->epoch = 0;
+    c->last_loss = p->loss;
+    if (c->mode != GCP_DIST_SYNC) {
+        c->tau = p->tau;
+        if (!c->server_set) {
+            c->server = p->adam;
+            c->server.rate = p->meta_rate > 0 ? p->meta_rate : p->adam.rate;
+        }
+    }
+    ST_TRY(server_reset(c));
+    double est;
+    ST_TRY(gcp_loss_estimate(c, p->loss, p->f_nz, p->f_z, p->fseed, &est));
+    c->best = est;
+    ST_TRY(checkpoint_save(c));
+    c->fit_active = true;
+    if (initial_est) *initial_est = est;
+    return GCP_OK;
+}
+
+gcp_status gcp_fit_epoch(gcp_ctx* c, double* est_out, int* accepted_out, int* done_out) {
+    ENTER(c);
+    if (!c->fit_active) return set_error(GCP_E_STATE, "gcp_fit_epoch: call gcp_fit_begin first");
+    const gcp_fit_params& p = c->fp;
+    if (c->epoch >= p.epochs || c->fails >= p.max_fails) {
+        if (done_out) *done_out = 1;
+        return GCP_OK;
+    }
+    gcp_adam_params ap = p.adam;
+    ap.rate = c->rate;
+    for (int i = 0; i < p.iters_per_epoch; ++i) {
+        ST_TRY(gcp_loss_grad(c, p.loss, nullptr));
+        ST_TRY(gcp_adam_step(c, &ap));
+    }
+    double est;
+    ST_TRY(gcp_loss_estimate(c, p.loss, p.f_nz, p.f_z, p.fseed, &est));
+    int accepted = est < c->best;
+    if (accepted) {
+        c->best = est;
+        ST_TRY(checkpoint_save(c));
+    } else {
+        ST_TRY(checkpoint_restore(c));
+        c->rate *= p.decay;
+        c->fails += 1;
+    }
+    c->epoch += 1;
+    if (est_out) *est_out = est;
+    if (accepted_out) *accepted_out = accepted;
+    if (done_out) *done_out = (c->epoch >= p.epochs || c->fails >= p.max_fails) ? 1 : 0;
+    return GCP_OK;
+}
+
+gcp_status gcp_fit(gcp_ctx* c, const gcp_fit_params* p, gcp_trace_fn trace, void* user, double* final_est_loss) {
+    ENTER(c);
+    const auto t0 = std::chrono::steady_clock::now();
+    double est;
+    ST_TRY(gcp_fit_begin(c, p, &est));
+    int done = p->epochs == 0;
+    while (!done) {
+        int acc;
+        ST_TRY(gcp_fit_epoch(c, &est, &acc, &done));
+        if (trace) {
+            const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            trace(user, c->epoch, (int64_t)c->it, est, c->rate, el);
+        }
+    }
+    if (final_est_loss) *final_est_loss = c->best;
+    c->fit_active = false;
+    return GCP_OK;
+}
+
+gcp_status gcp_counters(gcp_ctx* c, uint32_t* it, int64_t* t, int64_t* launches) {
+    if (!c) return set_error(GCP_E_ARG, "null context");
+    if (it) *it = c->it;
+    if (t) *t = c->t;
+    if (launches) *launches = c->launches;
+    return GCP_OK;
+}
+
+gcp_status gcp_profile_enable(gcp_ctx* c, int on) {
+    ENTER(c);
+    c->prof_on = on != 0;
+    return GCP_OK;
+}
+
+gcp_status gcp_profile_get(gcp_ctx* c, int which, double* ms, int64_t* launches, int reset) {
+    ENTER(c);
+    if (which < 0 || which >= PROF_N) return set_error(GCP_E_ARG, "gcp_profile_get: bad kernel class");
+    prof_resolve(c);
+    if (ms) *ms = c->prof_ms[which];
+    if (launches) *launches = c->prof_n[which];
+    if (reset) {
+        c->prof_ms[which] = 0;
+        c->prof_n[which] = 0;
+    }
+    return GCP_OK;
+}
+
+gcp_status gcp_grid_plan(int P, int d, const int64_t* dims, int* grid_out, int64_t* lo_out, int64_t* hi_out) {
+    if (P < 1 || d < 1 || d > kMaxModes || !dims || !grid_out) return set_error(GCP_E_ARG, "gcp_grid_plan: args");
+    for (int k = 0; k < d; ++k)
+        if (dims[k] < 1) return set_error(GCP_E_ARG, "gcp_grid_plan: dims");
+    // enumerate ordered divisor tuples in lexicographic order; strict < keeps the first minimum
+    int cur[kMaxModes];
+    double best = INFINITY;
+    std::vector<int> divs;
+    for (int n = 1; n <= P; ++n)
+        if (P % n == 0) divs.push_back(n);
+    std::vector<int> idx(d, 0);
+    for (;;) {
+        int64_t prod = 1;
+        for (int k = 0; k < d; ++k) prod *= divs[idx[k]];
+        if (prod == P) {
+            double obj = 0;
+            for (int k = 0; k < d; ++k) obj += (double)dims[k] * (double)(P / divs[idx[k]]);
+            if (obj < best) {
+                best = obj;
+                for (int k = 0; k < d; ++k) cur[k] = divs[idx[k]];
+            }
+        }
+        int k = d - 1;
+        while (k >= 0 && ++idx[k] == (int)divs.size()) idx[k--] = 0;
+        if (k < 0) break;
+    }
+    for (int k = 0; k < d; ++k) grid_out[k] = cur[k];
+    if (lo_out || hi_out) {
+        for (int w = 0; w < P; ++w) {
+            int rem = w, b[kMaxModes];
+            for (int k = d - 1; k >= 0; --k) {
+                b[k] = rem % cur[k];
+                rem /= cur[k];
+            }
+            for (int k = 0; k < d; ++k) {
+                const int64_t ck = (dims[k] + cur[k] - 1) / cur[k];
+                if (lo_out) lo_out[w * d + k] = std::min<int64_t>(b[k] * ck, dims[k]);
+                if (hi_out) hi_out[w * d + k] = std::min<int64_t>((b[k] + 1) * ck, dims[k]);
+            }
+        }
+    }
+    return GCP_OK;
+}
+
+}  // extern "C"

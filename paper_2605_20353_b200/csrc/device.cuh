@@ -1,0 +1,186 @@
+// device.cuh -- device-side building blocks of the sample kernels:
+// Philox4x32-10 counter RNG (reading R11), index maps, COO record fetch and the
+// hash-set membership probe, and the three losses (reading R3).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gcp_internal.h"
+
+namespace gcp {
+
+// ---- Philox4x32-10 ---------------------------------------------------------
+// Ten rounds of (c0,c1,c2,c3) -> (hi(M1 c2)^c1^k0, lo(M1 c2), hi(M0 c0)^c3^k1,
+// lo(M0 c0)); key bumped by the Weyl constants between rounds.
+struct U64x2 { uint64_t w0, w1; };
+
+__device__ __forceinline__ U64x2 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                        uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    U64x2 o;
+    o.w0 = (uint64_t)c0 | ((uint64_t)c1 << 32);
+    o.w1 = (uint64_t)c2 | ((uint64_t)c3 << 32);
+    return o;
+}
+
+// floor(W * n / 2^64): an exact integer map of a uniform 64-bit word onto [0, n).
+__device__ __forceinline__ uint64_t range_map(uint64_t W, uint64_t n) { return __umul64hi(W, n); }
+
+// ---- hashing ------------------------------------------------------------------
+__device__ __host__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64 finaliser
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t hash_key(uint64_t lo, uint64_t hi) { return mix64(lo ^ mix64(hi + 0x9E3779B97F4A7C15ull)); }
+
+constexpr uint64_t kEmpty = ~0ull;
+
+// Bucketised linear probing: a key hashes to a 32-byte bucket (4 u64 slots or
+// 2 u128 slots); insertion and lookup scan slots from the bucket start, so an
+// empty slot proves absence.  One 32-B sector per probe at load <= 0.5.
+__device__ __forceinline__ bool set_contains64(const uint64_t* __restrict__ h, uint64_t mask, uint64_t key) {
+    uint64_t s = (hash_key(key, 0) & mask) & ~3ull;
+    for (;;) {
+        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(h + s));
+        const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(h + s + 2));
+        if (a.x == key || a.y == key || b.x == key || b.y == key) return true;
+        if (a.x == kEmpty || a.y == kEmpty || b.x == kEmpty || b.y == kEmpty) return false;
+        s = (s + 4) & mask;
+    }
+}
+__device__ __forceinline__ bool set_contains128(const uint64_t* __restrict__ h, uint64_t mask,
+                                                uint64_t klo, uint64_t khi) {
+    // slots are (lo, hi) pairs: slot index s occupies h[2s], h[2s+1]
+    uint64_t s = (hash_key(klo, khi) & mask) & ~1ull;
+    for (;;) {
+        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(h + 2 * s));
+        const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(h + 2 * s + 2));
+        if ((a.x == klo && a.y == khi) || (b.x == klo && b.y == khi)) return true;
+        if ((a.x == kEmpty && a.y == kEmpty) || (b.x == kEmpty && b.y == kEmpty)) return false;
+        s = (s + 2) & mask;
+    }
+}
+
+// ---- losses (reading R3), in the kernel precision T -----------------------------
+template <typename T> __device__ __forceinline__ T d_log(T x);
+template <> __device__ __forceinline__ float d_log<float>(float x) { return logf(x); }
+template <> __device__ __forceinline__ double d_log<double>(double x) { return log(x); }
+template <typename T> __device__ __forceinline__ T d_log1p(T x);
+template <> __device__ __forceinline__ float d_log1p<float>(float x) { return log1pf(x); }
+template <> __device__ __forceinline__ double d_log1p<double>(double x) { return log1p(x); }
+template <typename T> __device__ __forceinline__ T d_exp(T x);
+template <> __device__ __forceinline__ float d_exp<float>(float x) { return expf(x); }
+template <> __device__ __forceinline__ double d_exp<double>(double x) { return exp(x); }
+
+template <typename T> __device__ __forceinline__ T sigmoid(T m) {
+    if (m >= T(0)) return T(1) / (T(1) + d_exp<T>(-m));
+    const T e = d_exp<T>(m);
+    return e / (T(1) + e);
+}
+
+// df/dm(x, m)
+template <typename T> __device__ __forceinline__ T loss_df(int loss, T x, T m) {
+    if (loss == GCP_LOSS_GAUSSIAN) return T(2) * (m - x);
+    if (loss == GCP_LOSS_POISSON) return T(1) - x / (m + T(1e-10));
+    return sigmoid<T>(m) - x;
+}
+// f(x, m)
+template <typename T> __device__ __forceinline__ T loss_f(int loss, T x, T m) {
+    if (loss == GCP_LOSS_GAUSSIAN) { const T e = x - m; return e * e; }
+    if (loss == GCP_LOSS_POISSON) return m - x * d_log<T>(m + T(1e-10));
+    const T sp = (m > T(0) ? m : T(0)) + d_log1p<T>(d_exp<T>(-fabs(m)));
+    return sp - x * m;
+}
+
+// ---- one sample: index generation, record fetch / probe (rows a1, a2) ------------
+template <typename T, int D>
+struct Sample {
+    uint32_t c[D];   // block-local coordinates
+    T x;             // data value (0 for zero samples)
+    int64_t j;       // canonical nonzero index, -1 for zeros
+    int attempts;
+    bool nz;
+};
+
+template <typename T> __device__ __forceinline__ T load_val(const uint32_t* r);
+template <> __device__ __forceinline__ float load_val<float>(const uint32_t* r) { return __uint_as_float(r[0]); }
+template <> __device__ __forceinline__ double load_val<double>(const uint32_t* r) {
+    return __hiloint2double((int)r[1], (int)r[0]);
+}
+
+// Draw the sample of local slot `s` (0 <= s < p: nonzero slot s; p <= s < p+q:
+// zero slot s-p).  Pure function of (seed, rank, kind, it, slot) and the tensor.
+template <typename T, int D>
+__device__ __forceinline__ Sample<T, D> draw_sample(const SampleArgs& a, int64_t s) {
+    Sample<T, D> o;
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    if (s < a.p) {
+        // nonzero slot: j uniform over [0, N) with replacement
+        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, a.it, k0, k1);
+        const int64_t j = (int64_t)range_map(w.w0, (uint64_t)a.N);
+        const uint32_t* r = a.rec + j * a.rec_words;
+        constexpr int VW = (int)(sizeof(T) / 4);   // value words at the record head
+        if (VW + D <= 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(r));
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+            o.x = load_val<T>(w4);
+#pragma unroll
+            for (int k = 0; k < D; ++k) o.c[k] = w4[(VW + k) & 3];
+        } else {
+            const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(r));
+            const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(r) + 1);
+            const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            o.x = load_val<T>(w8);
+#pragma unroll
+            for (int k = 0; k < D; ++k) o.c[k] = w8[(VW + k) & 7];
+        }
+        o.j = j;
+        o.attempts = 1;
+        o.nz = true;
+        return o;
+    }
+    // zero slot: draw d indices, reject while the candidate is a nonzero
+    const uint32_t zs = (uint32_t)(s - a.p);
+    o.x = T(0);
+    o.j = -1;
+    o.nz = false;
+    for (uint32_t att = 0;; ++att) {
+#pragma unroll
+        for (int g = 0; g < (D + 1) / 2; ++g) {
+            const U64x2 w = philox(zs, a.rank, (a.kind_z << 28) | (att << 4) | (uint32_t)g, a.it, k0, k1);
+            o.c[2 * g] = (uint32_t)range_map(w.w0, a.bdim[2 * g]);
+            if (2 * g + 1 < D) o.c[2 * g + 1] = (uint32_t)range_map(w.w1, a.bdim[2 * g + 1]);
+        }
+        o.attempts = (int)att + 1;
+        if (!a.stratified) break;
+        bool present;
+        if (!a.key128) {
+            uint64_t key = o.c[0];
+#pragma unroll
+            for (int k = 1; k < D; ++k) key = key * a.bdim[k] + o.c[k];
+            present = set_contains64(a.hash, a.hash_mask, key);
+        } else {
+            unsigned __int128 key = o.c[0];
+#pragma unroll
+            for (int k = 1; k < D; ++k) key = key * a.bdim[k] + o.c[k];
+            present = set_contains128(a.hash, a.hash_mask, (uint64_t)key, (uint64_t)(key >> 64));
+        }
+        if (!present) break;
+        if (att + 1 >= (uint32_t)kRejectCap) {
+            atomicMin(a.err_slot, (unsigned long long)zs);
+            break;
+        }
+    }
+    return o;
+}
+
+}  // namespace gcp

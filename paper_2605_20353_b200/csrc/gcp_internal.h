@@ -1,0 +1,169 @@
+// gcp_internal.h -- context layout and host helpers shared by the csrc/*.cu
+// translation units of libgcp.so.  Not part of the ABI (see include/gcp.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gcp.h"
+
+namespace gcp {
+
+constexpr int kMaxModes = 8;          // array capacity
+constexpr int kMaxD = 6;              // d <= 6 on the device path (record = value + d coords <= 32 B)
+constexpr int kRejectCap = 1000;      // reading R5
+constexpr int kBlock = 256;           // threads per CTA of the sample kernels
+constexpr int kSampleMinBlocks = 2;   // >= 16 resident warps per SM (register cap 128)
+constexpr double kHashLoad = 0.5;     // target hash-set load factor
+
+enum Kind : uint32_t { KIND_GRAD_NZ = 0, KIND_GRAD_Z = 1, KIND_F_NZ = 2, KIND_F_Z = 3, KIND_INIT = 4 };
+enum Prof { PROF_GRAD = 0, PROF_ADAM = 1, PROF_LOSS = 2, PROF_COMM = 3, PROF_OTHER = 4, PROF_N = 5 };
+
+// Everything the sample kernels (K2 gradient / loss mode, export) need.
+struct SampleArgs {
+    const uint32_t* rec;      // AoS records: [value (1 or 2 words)][d local coords u32][pad]
+    int rec_words;            // stride in 32-bit words (4 or 8)
+    int val_words;            // 1 (fp32) or 2 (fp64)
+    int64_t N;                // local nonzeros
+    const uint64_t* hash;     // open-addressing set (u64 keys, or u128 as lo,hi pairs)
+    uint64_t hash_mask;       // slots - 1 (power of two)
+    int key128;               // 1: 128-bit keys
+    uint32_t bdim[kMaxModes]; // block extent per mode (hi_k - lo_k)
+    int64_t p, q;             // local nonzero / zero slots in this launch
+    uint64_t seed;
+    uint32_t rank, it, kind_nz, kind_z;
+    int stratified;           // 0: semi-stratified (no membership test)
+    unsigned long long* err_slot;  // min zero slot that hit the rejection cap (ULLONG_MAX = none)
+};
+
+struct ModelArgs {
+    const void* A;            // factor array (T), mode-major, rows padded to R_pad
+    void* G;                  // gradient array, same layout
+    const void* lambda;       // R_pad values (T), zero padded
+    int64_t off[kMaxModes];   // element offset of mode k
+    int R_pad;
+};
+
+struct Segment {              // contiguous ranges of the coefficient arrays (Adam)
+    int64_t start[2 * kMaxModes];
+    int64_t len[2 * kMaxModes];
+    int n;
+};
+
+}  // namespace gcp
+
+struct gcp_ctx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    gcp_precision prec = GCP_FP32;
+    int sm_count = 148;
+    int tsize = 4;                      // sizeof(T)
+    // ---- error state
+    gcp_status sticky = GCP_OK;
+    // ---- distribution
+    int P = 1, rank = 0;
+    gcp_dist_mode mode = GCP_DIST_SYNC;
+    int grid[gcp::kMaxModes] = {0};
+    bool grid_given = false;
+    bool dist_ready = false;
+    ncclComm_t world = nullptr;
+    ncclComm_t slice[gcp::kMaxModes] = {nullptr};
+    int slice_size[gcp::kMaxModes] = {0}, slice_rank[gcp::kMaxModes] = {0};
+    int64_t tau = 0;
+    gcp_adam_params server{};
+    bool server_set = false;
+    // ---- tensor
+    bool have_tensor = false;
+    int d = 0;
+    int64_t dims[gcp::kMaxModes] = {0}, lo[gcp::kMaxModes] = {0}, hi[gcp::kMaxModes] = {0};
+    int64_t N = 0, N_global = 0;
+    unsigned __int128 M = 0;            // local block entries
+    bool any_zero_global = true;        // some rank has M_w > N_w
+    uint32_t* d_rec = nullptr;
+    int rec_words = 4, val_words = 1;
+    uint64_t* d_hash = nullptr;
+    uint64_t hash_slots = 0;
+    int key128 = 0;
+    // ---- model
+    bool have_model = false;
+    int R = 0, R_pad = 0;
+    int64_t rows[gcp::kMaxModes] = {0};     // allocated rows per mode (>= block rows, multiple of slice size)
+    int64_t off[gcp::kMaxModes] = {0};      // element offsets
+    int64_t n_coef = 0;
+    void *d_A = nullptr, *d_G = nullptr, *d_B = nullptr, *d_C = nullptr, *d_lambda = nullptr;
+    void *d_Ack = nullptr, *d_Bck = nullptr, *d_Cck = nullptr;   // fit checkpoint
+    void *d_U = nullptr, *d_Bs = nullptr, *d_Cs = nullptr;       // FedAdam server copy + state
+    int64_t t = 0, t_ck = 0, ts = 0, ts_ck = 0;
+    uint32_t it = 0;
+    bool have_grad = false;
+    int last_loss = 0;
+    // ---- sampler binding
+    bool bound = false;
+    gcp_strategy strategy = GCP_STRATIFIED;
+    int64_t s_nz = 0, s_z = 0, p_w = 0, q_w = 0;
+    uint64_t seed = 0;
+    // ---- scratch
+    double* d_partials = nullptr;       // per-CTA fp64 partial sums
+    int partials_cap = 0;
+    double* h_scalar = nullptr;         // pinned
+    unsigned long long* d_err = nullptr;
+    unsigned long long* h_err = nullptr;  // pinned
+    int grad_blocks = 0;                // persistent grid of the sample kernels
+    // ---- fit state
+    bool fit_active = false;
+    gcp_fit_params fp{};
+    double best = 0, rate = 0;
+    int fails = 0, epoch = 0;
+    // ---- instrumentation
+    int64_t launches = 0;
+    bool prof_on = false;
+    struct PendingEv { cudaEvent_t a, b; int which; };
+    std::vector<PendingEv> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[gcp::PROF_N] = {0};
+    int64_t prof_n[gcp::PROF_N] = {0};
+};
+
+namespace gcp {
+
+// thread-local error message + status helpers (api.cu)
+gcp_status set_error(gcp_status st, const std::string& msg);
+gcp_status cuda_fail(gcp_ctx* c, cudaError_t e, const char* what);
+gcp_status nccl_fail(gcp_ctx* c, ncclResult_t r, const char* what);
+
+// launch bracketing for the profiler and the launch counter
+void prof_begin(gcp_ctx* c, int which, cudaEvent_t* ev);
+void prof_end(gcp_ctx* c, int which, cudaEvent_t ev);
+
+// kernels.cu launchers (enqueue on c->stream; return cudaGetLastError())
+cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss,
+                                 int loss_mode, int semi_nz, double w_nz, double w_z, int with_loss,
+                                 double* partials, int nblocks);
+cudaError_t launch_reduce_partials(gcp_ctx* c, const double* partials, int n, double* out);
+cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
+                          const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);
+cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C,
+                        double rate, double beta1, double beta2, double eps, double lower,
+                        int64_t t, int zero_g);
+cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
+cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
+cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);
+int sample_kernel_blocks(gcp_ctx* c);
+
+// ingest.cu
+gcp_status ingest(gcp_ctx* c, const gcp_ctx* geom, int64_t nnz, const int64_t* subs, const double* vals);
+cudaError_t launch_contains(gcp_ctx* c, int64_t n, const int64_t* coords_dev, int8_t* out_dev);
+
+// dist.cu
+gcp_status dist_make_slices(gcp_ctx* c);
+gcp_status dist_sync_exchange_pre(gcp_ctx* c);     // reduce-scatter G
+gcp_status dist_sync_exchange_post(gcp_ctx* c);    // all-gather A
+gcp_status dist_async_sync(gcp_ctx* c);            // Alg. 3 averaging / Alg. 4 server step
+gcp_status dist_allreduce_scalar(gcp_ctx* c, double* dev_scalar);
+gcp_status dist_allreduce_i64_host(gcp_ctx* c, int64_t* v, int n);
+
+}  // namespace gcp

@@ -1,0 +1,284 @@
+// kernels.cuh -- the device kernels of the hot path, templated on the
+// arithmetic type T (float / double), the number of modes D, and the lane
+// geometry of a sample (GL lanes x NV 16-byte vectors cover one factor row).
+//
+//   k_sample  (K2)  rows a1-a5 fused: Philox draw -> record fetch or hash probe
+//                   -> gather d rows -> m -> y = w df/dm -> per-mode scatter-add.
+//                   loss_mode = 1 turns it into the f-sample loss estimate (a9):
+//                   same draw and gather, accumulates w f(x, m), no scatter.
+//   k_export        test-only: the same draws, written out as indices.
+//   k_adam    (K3)  Alg. 1 over contiguous segments, G reset fused (a7).
+//   k_init    (K0)  Philox U[0,1) factor initialisation (reading R12).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+
+namespace gcp {
+
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
+template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+
+template <typename T> struct KParams {
+    int loss;
+    int loss_mode;    // 1: loss estimate only (no scatter)
+    int semi_nz;      // 1: semi-stratified nonzero value w (f'(x,m) - f'(0,m))
+    int with_loss;    // accumulate sum w f(x, m)
+    T w_nz, w_z;
+    double* partials; // per-CTA fp64 partial of sum w f
+};
+
+__device__ __forceinline__ void red_add_v(float* p, const float (&v)[4]) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3])
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_v(double* p, const double (&v)[2]) {
+    atomicAdd(p, v[0]);
+    atomicAdd(p + 1, v[1]);
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void ldg_vec(T (&dst)[N], const T* src);
+template <>
+__device__ __forceinline__ void ldg_vec<float, 4>(float (&dst)[4], const float* src) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+    dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void ldg_vec<double, 2>(double (&dst)[2], const double* src) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(src));
+    dst[0] = v.x; dst[1] = v.y;
+}
+
+// One warp takes 32 consecutive slots: each lane draws one sample (index work
+// is per thread, so Philox and the probe run once per sample), then the warp
+// processes the 32 samples in GL rounds of 32/GL samples, a sample per group of
+// GL lanes, each lane owning NV 16-byte vectors of every factor row.  Rounds are
+// handled RB at a time with all their row loads issued before any arithmetic.
+template <typename T, int D, int GL, int NV>
+__global__ void __launch_bounds__(kBlock, kSampleMinBlocks) k_sample(const SampleArgs sa, const ModelArgs ma,
+                                                   const KParams<T> kp) {
+    constexpr int VE = Vec16<T>::n;
+    constexpr int SPR = 32 / GL;                 // samples per round
+    // rounds per load batch: bounded so the row registers (RB*D*NV*16 B) stay < ~64 regs
+    // (a power of two, so it divides GL)
+    constexpr int RB_REG = 8 / (D * NV);
+    constexpr int RB_CAP = GL < 4 ? GL : 4;
+    constexpr int RB = RB_REG >= 4 && RB_CAP >= 4 ? 4 : (RB_REG >= 2 && RB_CAP >= 2 ? 2 : 1);
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / GL, gl = lane % GL;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = sa.p + sa.q;
+    const int64_t nchunks = (total + 31) >> 5;
+    const T* __restrict__ A = static_cast<const T*>(ma.A);
+    T* __restrict__ G = static_cast<T*>(ma.G);
+    const int R_pad = ma.R_pad;
+
+    // this lane's slice of lambda (zero beyond R)
+    T lam[NV][VE];
+    bool vok[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const int col = (gl + v * GL) * VE;
+        vok[v] = col < R_pad;
+        if (vok[v]) ldg_vec<T, VE>(lam[v], static_cast<const T*>(ma.lambda) + col);
+        else {
+#pragma unroll
+            for (int e = 0; e < VE; ++e) lam[v][e] = T(0);
+        }
+    }
+
+    double lacc = 0.0;
+    for (int64_t chunk = warp0; chunk < nchunks; chunk += nwarps) {
+        const int64_t s = (chunk << 5) + lane;
+        const bool valid = s < total;
+        Sample<T, D> smp;
+        if (valid) smp = draw_sample<T, D>(sa, s);
+        else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) smp.c[k] = 0;
+            smp.x = T(0); smp.nz = false;
+        }
+        const T wv = smp.nz ? kp.w_nz : kp.w_z;
+        const int flags = (valid ? 1 : 0) | (smp.nz ? 2 : 0);
+
+#pragma unroll
+        for (int r0 = 0; r0 < GL; r0 += RB) {
+            uint32_t rc[RB][D];
+            T rx[RB], rw[RB];
+            int rf[RB];
+            T a[RB][D][NV][VE];
+            // ---- phase 1: fetch this batch's samples and issue every row load
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
+                const int src = (r0 + b) * SPR + grp;
+#pragma unroll
+                for (int k = 0; k < D; ++k) rc[b][k] = __shfl_sync(0xffffffffu, smp.c[k], src);
+                rx[b] = __shfl_sync(0xffffffffu, smp.x, src);
+                rw[b] = __shfl_sync(0xffffffffu, wv, src);
+                rf[b] = __shfl_sync(0xffffffffu, flags, src);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const T* row = A + ma.off[k] + (int64_t)rc[b][k] * R_pad;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        if ((rf[b] & 1) && vok[v]) ldg_vec<T, VE>(a[b][k][v], row + (gl + v * GL) * VE);
+                        else {
+#pragma unroll
+                            for (int e = 0; e < VE; ++e) a[b][k][v][e] = T(0);
+                        }
+                    }
+                }
+            }
+            // ---- phase 2: model value, derivative, scatter
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
+                T mpart = T(0);
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) {
+                        T p = lam[v][e];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) p *= a[b][k][v][e];
+                        mpart += p;
+                    }
+#pragma unroll
+                for (int o = GL / 2; o > 0; o >>= 1) mpart += __shfl_xor_sync(0xffffffffu, mpart, o);
+                const T m = mpart;
+                const bool ok = rf[b] & 1, isnz = rf[b] & 2;
+                T y;
+                if (kp.semi_nz && isnz) y = rw[b] * (loss_df<T>(kp.loss, rx[b], m) - loss_df<T>(kp.loss, T(0), m));
+                else y = rw[b] * loss_df<T>(kp.loss, rx[b], m);
+                if (kp.with_loss && ok && gl == 0) lacc += (double)(rw[b] * loss_f<T>(kp.loss, rx[b], m));
+                if (!kp.loss_mode && ok) {
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        T* grow = G + ma.off[k] + (int64_t)rc[b][k] * R_pad;
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            if (!vok[v]) continue;
+                            T cv[VE];
+#pragma unroll
+                            for (int e = 0; e < VE; ++e) {
+                                T z = y * lam[v][e];
+#pragma unroll
+                                for (int j = 0; j < D; ++j)
+                                    if (j != k) z *= a[b][j][v][e];
+                                cv[e] = z;
+                            }
+                            red_add_v(grow + (gl + v * GL) * VE, cv);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (kp.with_loss) {
+        // deterministic CTA reduction of the per-thread fp64 partials
+        __shared__ double red[kBlock / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, o);
+        if (lane == 0) red[threadIdx.x >> 5] = lacc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kBlock / 32; ++w) t += red[w];
+            kp.partials[blockIdx.x] = t;
+        }
+    }
+}
+
+template <typename T, int D>
+__global__ void k_export(const SampleArgs sa, int64_t first, int64_t count, const int64_t* lo,
+                         int64_t* subs, int64_t* jout, int32_t* att) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const Sample<T, D> smp = draw_sample<T, D>(sa, first + i);
+#pragma unroll
+    for (int k = 0; k < D; ++k) subs[i * D + k] = lo[k] + (int64_t)smp.c[k];
+    if (jout) jout[i] = smp.j;
+    if (att) att[i] = smp.attempts;
+}
+
+// Alg. 1 over the segments of the contiguous arrays:
+// B <- b1 B + (1-b1) g; C <- b2 C + (1-b2) g^2; A <- A - rate (B bc1)/sqrt(C bc2 + eps);
+// A <- (A < l) ? l : A; G <- 0 (fused reset).  bc = 1/(1-beta^t) from the host in fp64.
+template <typename T>
+__global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
+                                              T* __restrict__ G, T* __restrict__ B, T* __restrict__ C,
+                                              T rate, T b1, T b2, T eps, T bc1, T bc2, T lower,
+                                              int zero_g) {
+    using V = typename Vec16<T>::type;
+    constexpr int VE = Vec16<T>::n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec_total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        // map the virtual vector index onto its segment
+        int64_t rem = i;
+        int sidx = 0;
+        while (sidx < seg.n - 1 && rem >= seg.len[sidx] / VE) { rem -= seg.len[sidx] / VE; ++sidx; }
+        const int64_t e = seg.start[sidx] + rem * VE;
+        V g = *reinterpret_cast<const V*>(G + e);
+        V a = *reinterpret_cast<const V*>(A + e);
+        V b = *reinterpret_cast<const V*>(B + e);
+        V c = *reinterpret_cast<const V*>(C + e);
+        T* gp = reinterpret_cast<T*>(&g);
+        T* ap = reinterpret_cast<T*>(&a);
+        T* bp = reinterpret_cast<T*>(&b);
+        T* cp = reinterpret_cast<T*>(&c);
+#pragma unroll
+        for (int q = 0; q < VE; ++q) {
+            const T gv = gp[q];
+            bp[q] = b1 * bp[q] + (T(1) - b1) * gv;
+            cp[q] = b2 * cp[q] + (T(1) - b2) * gv * gv;
+            T av = ap[q] - rate * ((bp[q] * bc1) / sqrt(cp[q] * bc2 + eps));
+            ap[q] = (av < lower) ? lower : av;
+        }
+        *reinterpret_cast<V*>(A + e) = a;
+        *reinterpret_cast<V*>(B + e) = b;
+        *reinterpret_cast<V*>(C + e) = c;
+        if (zero_g) {
+            V z;
+            T* zp = reinterpret_cast<T*>(&z);
+#pragma unroll
+            for (int q = 0; q < VE; ++q) zp[q] = T(0);
+            *reinterpret_cast<V*>(G + e) = z;
+        }
+    }
+}
+
+struct InitArgs {
+    int d, R, R_pad;
+    int64_t rows[kMaxModes], bdim[kMaxModes], lo[kMaxModes], off[kMaxModes], goff[kMaxModes];
+    int64_t n_coef;
+    uint64_t seed;
+};
+
+// Factor k, local row i, column r < R: global element e = goff_k + (lo_k + i) R + r of the
+// unpadded mode-major concatenation; value (W0 >> 11) 2^-53 of Philox(lo32 e, hi32 e, 4<<28, 0).
+template <typename T>
+__global__ void k_init(const InitArgs ia, T* __restrict__ A) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < ia.n_coef;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (k < ia.d - 1 && x >= ia.off[k + 1]) ++k;
+        const int64_t loc = x - ia.off[k];
+        const int64_t i = loc / ia.R_pad;
+        const int r = (int)(loc % ia.R_pad);
+        T v = T(0);
+        if (r < ia.R && i < ia.bdim[k]) {
+            const uint64_t e = (uint64_t)(ia.goff[k] + (ia.lo[k] + i) * ia.R + r);
+            const U64x2 w = philox((uint32_t)e, (uint32_t)(e >> 32), (uint32_t)KIND_INIT << 28, 0u,
+                                   (uint32_t)ia.seed, (uint32_t)(ia.seed >> 32));
+            v = (T)((double)(w.w0 >> 11) * 0x1.0p-53);
+        }
+        A[x] = v;
+    }
+}
+
+}  // namespace gcp

@@ -1,0 +1,240 @@
+"""GPU parity: libgcp.so (through the C ABI) against the fp64 oracle.
+
+Bit-exact: sample coordinates, nonzero indices j, attempt counts, canonical
+order, hash membership, factor initialisation (fp32 = round(fp64)).
+Tolerance: gradients per element |dG| <= tol * S (S = the
+oracle's rounding-scale sum) and per mode ||dG||_F <= tol ||G||_F, with
+tol = 1e-4 (fp32) / 1e-10 (fp64); loss estimates |dF| <= tol * sum|terms|.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gcp_synth
+
+pytestmark = pytest.mark.gpu
+
+LOSSES = ["gaussian", "poisson", "bernoulli"]
+TOL = {"fp32": 1e-4, "fp64": 1e-10}
+
+
+@pytest.fixture(scope="module")
+def gcp():
+    import paper_2605_20353_b200 as g
+    return g
+
+
+def _tensor(loss, dims=(20, 30, 40), nnz=2400, seed=1001):
+    subs, vals = gcp_synth.chi_kolda(dims, nnz, 4, seed, loss=loss)
+    subs, vals = subs.numpy(), vals.numpy()
+    if loss == "gaussian":
+        vals = vals - 1.5  # signed data
+    return subs, vals
+
+
+def _ctx(gcp, dims, subs, vals, prec="fp32", R=4, mseed=2001):
+    c = gcp.Context(0, None, prec)
+    c.tensor_create(dims, subs, vals)
+    c.model_init(R, mseed)
+    return c
+
+
+def _model(c, d):
+    return [c.model_get(k) for k in range(d)]
+
+
+def test_canonical_order_and_membership(gcp, orc):
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals)
+    t = orc.Tensor(dims, subs, vals)
+    ss, sv = t.sorted()
+    gs, gv = c.tensor_export_sorted(0, len(vals))
+    assert np.array_equal(gs, ss) and np.array_equal(gv, sv.astype(np.float32).astype(np.float64))
+    assert c.tensor_contains(subs).all()
+    rng = np.random.default_rng(0)
+    cand = np.stack([rng.integers(0, I, 20000) for I in dims], 1)
+    want = np.array([t.contains(x) for x in cand])
+    assert np.array_equal(c.tensor_contains(cand), want)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_factor_init_bit_exact(gcp, orc, prec):
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals, prec=prec, R=5)
+    A = orc.factor_init(2001, dims, 5)
+    for k in range(3):
+        want = A[k].astype(np.float32).astype(np.float64) if prec == "fp32" else A[k]
+        assert np.array_equal(c.model_get(k), want)
+
+
+@pytest.mark.parametrize("strategy", ["stratified", "semi"])
+def test_sample_indices_bit_exact(gcp, orc, strategy):
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals)
+    t = orc.Tensor(dims, subs, vals)
+    p, q = 1000, 1000
+    for it in range(3):
+        c.sample(strategy, p, q, 3001)
+        for stratum, n in ((0, p), (1, q)):
+            gs, gj, gw, ga = c.sample_export(stratum, 0, n)
+            os_, oj, ow, oa = orc.sample_export(t, stratum, 3001, 0, it, n, 0, n, strategy=strategy)
+            assert np.array_equal(gs, os_)
+            assert np.array_equal(gj, oj)
+            assert np.array_equal(ga, oa)
+            assert np.array_equal(gw, ow)
+        if stratum == 1 and strategy == "stratified":
+            assert oa.max() > 1  # rejection really fired at rho = 0.1
+        # advance the iteration counter (it) by one Adam step
+        c.loss_grad("poisson")
+        c.adam_step()
+
+
+def _grad_check(G, Go, S, tol, label):
+    for k, (g, go, s) in enumerate(zip(G, Go, S)):
+        diff = np.abs(g - go)
+        bad = diff > tol * s + 1e-300
+        assert not bad.any(), f"{label} mode {k}: {bad.sum()} elements, worst {diff[bad].max()} vs {s[bad].max()}"
+        assert np.linalg.norm(g - go) <= tol * np.linalg.norm(go) + 1e-300, label
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("strategy", ["stratified", "semi"])
+@pytest.mark.parametrize("loss", LOSSES)
+def test_gradient_parity(gcp, orc, loss, strategy, prec):
+    dims = (20, 30, 40)
+    subs, vals = _tensor(loss)
+    c = _ctx(gcp, dims, subs, vals, prec=prec)
+    if loss == "bernoulli":  # centre the model so sigma(m) is not saturated
+        for k in range(3):
+            c.model_set(k, c.model_get(k) - 0.5)
+    t = orc.Tensor(dims, subs, vals)
+    p, q = 1000, 1000
+    c.sample(strategy, p, q, 3001)
+    A = _model(c, 3)
+    ls = c.loss_grad(loss, want_loss=True)
+    G = [c.grad_get(k) for k in range(3)]
+    Go, S, lo = orc.sampled_grad(t, A, loss, 3001, 0, 0, p, q, strategy)
+    _grad_check(G, Go, S, TOL[prec], f"{loss}/{strategy}/{prec}")
+    # sampled loss sum_s w f: relative to the sum of |w f| scales
+    assert abs(ls - lo) <= TOL[prec] * max(1.0, abs(lo)) * 10
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("loss", LOSSES)
+def test_loss_estimate_parity(gcp, orc, loss, prec):
+    dims = (20, 30, 40)
+    subs, vals = _tensor(loss)
+    c = _ctx(gcp, dims, subs, vals, prec=prec)
+    t = orc.Tensor(dims, subs, vals)
+    A = _model(c, 3)
+    est = c.loss_estimate(loss, 2000, 2000, 4001)
+    oe, scale = orc.loss_estimate(t, A, loss, 4001, 0, 2000, 2000)
+    assert abs(est - oe) <= TOL[prec] * scale
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_adam_parity_from_identical_gradient(gcp, orc, prec):
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals, prec=prec)
+    c.sample("stratified", 1000, 1000, 3001)
+    A = np.concatenate([a.ravel() for a in _model(c, 3)])
+    B = np.zeros_like(A)
+    Cm = np.zeros_like(A)
+    for step in range(1, 4):
+        c.loss_grad("poisson")
+        G = np.concatenate([c.grad_get(k).ravel() for k in range(3)])
+        p = gcp.adam_params(rate=1e-2, beta1=0.9, beta2=0.999, eps=1e-8)
+        c.adam_step(p)
+        orc.adam(A, G, B, Cm, step, 1e-2, 0.9, 0.999, 1e-8, 0.0)
+        Ag = np.concatenate([a.ravel() for a in _model(c, 3)])
+        tol = TOL[prec]
+        assert np.all(np.abs(Ag - A) <= tol * np.maximum(np.abs(A), 1.0) * 10 + 1e-4 * 1e-2 * (prec == "fp32"))
+        A = Ag.copy()  # continue from the GPU state (identical-state protocol, C18)
+        assert (Ag >= 0).all()  # Poisson clamp l = 0
+    ctr = c.counters()
+    assert ctr["it"] == 3 and ctr["t"] == 3
+
+
+def test_zero_gradient_and_errors(gcp):
+    dims = (2, 2, 2)
+    full = np.array(np.unravel_index(np.arange(8), dims)).T
+    c = gcp.Context(0, None, "fp32")
+    with pytest.raises(gcp.GcpError) as e:
+        c.tensor_create(dims, np.array([[0, 0, 0], [0, 0, 0]]), np.array([1.0, 2.0]))
+    assert e.value.name == "GCP_E_DUP"
+    with pytest.raises(gcp.GcpError) as e:
+        c.tensor_create(dims, np.array([[0, 2, 0]]), np.array([1.0]))
+    assert e.value.name == "GCP_E_RANGE"
+    with pytest.raises(gcp.GcpError) as e:
+        c.tensor_create(dims, np.array([[0, 1, 0]]), np.array([np.inf]))
+    assert e.value.name == "GCP_E_ARG"
+    c.tensor_create(dims, full, np.ones(8))
+    with pytest.raises(gcp.GcpError) as e:
+        c.sample("stratified", 10, 10, 1)
+    assert e.value.name == "GCP_E_NO_ZEROS"
+    with pytest.raises(gcp.GcpError) as e:
+        c.loss_grad("poisson")
+    assert e.value.name == "GCP_E_STATE"
+    # one zero in 10^4 entries: the rejection cap fires (reading R5) and is sticky
+    dims = (10, 10, 100)
+    lin = np.arange(10 * 10 * 100)[1:]
+    c2 = gcp.Context(0, None, "fp32")
+    c2.tensor_create(dims, np.array(np.unravel_index(lin, dims)).T, np.ones(len(lin)))
+    c2.model_init(2, 1)
+    c2.sample("stratified", 10, 10, 1)
+    with pytest.raises(gcp.GcpError) as e:
+        c2.loss_grad("poisson", want_loss=True)
+    assert e.value.name == "GCP_E_REJECT_CAP"
+    with pytest.raises(gcp.GcpError) as e:
+        c2.model_get(0)
+    assert e.value.name == "GCP_E_STATE"
+
+
+def test_u128_keys_lbnl_shape(gcp, orc):
+    """c3's 5-way shape has M = 4.0e19 > 2^64: 128-bit keys on the device."""
+    dims = gcp_synth.CONFIGS["c3"]["dims"]
+    assert math.prod(dims) > 2 ** 64
+    rng = np.random.default_rng(5)
+    n = 20000
+    subs = np.unique(np.stack([rng.integers(0, I, n) for I in dims], 1), axis=0)
+    vals = np.ones(len(subs))
+    c = _ctx(gcp, dims, subs, vals, R=10)
+    t = orc.Tensor(dims, subs, vals)
+    assert c.tensor_contains(subs).all()
+    cand = np.stack([rng.integers(0, I, 5000) for I in dims], 1)
+    cand[:2000] = subs[:2000]
+    assert np.array_equal(c.tensor_contains(cand), np.array([t.contains(x) for x in cand]))
+    c.sample("stratified", 3000, 3000, 3003)
+    for stratum in (0, 1):
+        gs, gj, _, ga = c.sample_export(stratum, 0, 3000)
+        os_, oj, _, oa = orc.sample_export(t, stratum, 3003, 0, 0, 3000, 0, 3000)
+        assert np.array_equal(gs, os_) and np.array_equal(gj, oj) and np.array_equal(ga, oa)
+    A = _model(c, 5)
+    for k in range(5):
+        c.model_set(k, A[k] - 0.4)
+    A = _model(c, 5)
+    c.loss_grad("bernoulli")
+    G = [c.grad_get(k) for k in range(5)]
+    Go, S, _ = orc.sampled_grad(t, A, "bernoulli", 3003, 0, 0, 3000, 3000)
+    _grad_check(G, Go, S, 1e-4, "u128 bernoulli")
+
+
+def test_fit_runs_and_decreases(gcp, orc):
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals)
+    t = orc.Tensor(dims, subs, vals)
+    A0 = _model(c, 3)
+    F0, _ = orc.loss_estimate(t, A0, "poisson", 2, 0, 2000, 2000)
+    p = c.fit_params(epochs=5, iters_per_epoch=20, s_nz=500, s_z=500, f_nz=2000, f_z=2000, loss="poisson",
+                     seed=7, fseed=2, rate=1e-2)
+    best, rows = c.fit(p)
+    assert len(rows) >= 3
+    assert best < F0
+    ests = [r[2] for r in rows]
+    assert min(ests) == pytest.approx(best)
