@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""GCP-Adam epoch benchmark (BASELINE.json metric) on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one GCP-Adam epoch: 100 x [fused sampling-MTTKRP (K2),
+(P>1 sync: reduce-scatter), Adam (K3), (P>1 sync: all-gather)] + the fixed-set
+loss estimate + the accept/reject decision -- every row of SURVEY §8(a).  The
+tensor is ingested and the model initialised before timing (inputs resident in
+HBM).  W untimed warm-up epochs, then K epochs between barrier + synchronize,
+CUDA events on the library's stream, max over ranks.  One JSON line on rank 0.
+
+--impl reference times the fp64 CPU oracle (the base contract's reference
+arm for this tier) on a bounded sample of the same workload, extrapolated to
+an epoch; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gcp_synth  # noqa: E402
+
+METRIC = "GCP-Adam epochs/sec and sampled-gradient samples/sec (1/2/4/8 B200); HBM GB/s"
+ITERS = 100  # iterations per epoch
+
+
+def workload(name):
+    c = gcp_synth.CONFIGS[name]
+    d = len(c["dims"])
+    M = math.prod(c["dims"])
+    rho = c["nnz"] / M
+    kB = 16 if M >= 2 ** 64 else 8
+    R = c["R"]
+    nz_b = (d + 1) * 4 + d * R * 4 + 2 * d * R * 4
+    z_b = kB / (1 - rho) + 3 * d * R * 4
+    desc = {"c1": "3-way 20x30x40 synthetic count tensor, ~2.4K nnz, R=4, Poisson",
+            "c2": "3-way 10Kx10Kx10K synthetic Poisson tensor, 100M nnz, R=16, stratified, p=q=1e7",
+            "c3": "5-way LBNL-network-shaped tensor, 1.7M nnz, R=10, Bernoulli-logit, p=q=1e6",
+            "c4": "3-way Amazon-reviews-shaped tensor, 1.74B nnz, R=16, Gaussian, p=q=1e7",
+            "c5": "3-way Reddit-2015-shaped tensor, 4.69B nnz, R=32, Poisson, p=q=1e8"}[name]
+    return dict(c, d=d, M=M, rho=rho, nz_bytes=nz_b, z_bytes=z_b, desc=desc)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """SM clock + clock-event (throttle) reasons sampled every 20 ms during the
+    timed region through NVML (the data of the recipe's nvidia-smi clocks line)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.sm, self.reasons, self.max = [], set(), None
+        self.stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = dev_index(self.dev)
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception:
+            self.nv = None
+        return self
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 20 ms"}
+
+
+def dev_index(local):
+    """Physical index of the local CUDA device (honours CUDA_VISIBLE_DEVICES)."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [x.strip() for x in vis.split(",") if x.strip()]
+        if local < len(ids) and ids[local].isdigit():
+            return int(ids[local])
+    return local
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(ws, x):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bcast_bytes(ws, rank, b):
+    if ws == 1:
+        return b
+    import torch.distributed as dist
+    obj = [b if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+# ------------------------------------------------------------------ data
+def make_tensor(name, device):
+    w = workload(name)
+    t0 = time.time()
+    subs, vals = gcp_synth.chi_kolda(w["dims"], w["nnz"], w["R"], gcp_synth.SEEDS[name]["data"], w["loss"],
+                                     device=device)
+    return subs, vals, time.time() - t0
+
+
+def block_of(subs, vals, lo, hi):
+    m = torch.ones(len(vals), dtype=torch.bool, device=vals.device)
+    for k in range(subs.shape[1]):
+        m &= (subs[:, k] >= int(lo[k])) & (subs[:, k] < int(hi[k]))
+    return subs[m], vals[m]
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+def run_oracle_sample(name, subs_h, vals_h, steps, warmup, sample_n):
+    """Time the fp64 oracle, as it stands, on a bounded sample of one epoch of
+    workload `name`: per step one sampled gradient with p'=q'=sample_n, one Adam
+    pass over all coefficients, one loss estimate with f'=sample_n; extrapolated
+    to the epoch (100 iterations at p=q, f-samples f)."""
+    import oracle
+    w = workload(name)
+    t0 = time.time()
+    t = oracle.Tensor(w["dims"], subs_h, vals_h)
+    setup = time.time() - t0
+    A = oracle.factor_init(gcp_synth.SEEDS[name]["model"], w["dims"], w["R"])
+    flat = np.concatenate([a.ravel() for a in A])
+    B, Cm = np.zeros_like(flat), np.zeros_like(flat)
+    times = []
+    for s in range(warmup + steps):
+        t1 = time.perf_counter()
+        G, _, _ = oracle.sampled_grad(t, A, w["loss"], gcp_synth.SEEDS[name]["sample"], 0, s, sample_n, sample_n,
+                                      with_scale=False)
+        tg = time.perf_counter() - t1
+        Gf = np.concatenate([g.ravel() for g in G])
+        t2 = time.perf_counter()
+        oracle.adam(flat, Gf, B, Cm, s + 1, 1e-3, 0.9, 0.999, 1e-8, oracle.loss_lower(w["loss"]))
+        ta = time.perf_counter() - t2
+        t3 = time.perf_counter()
+        oracle.loss_estimate(t, A, w["loss"], 2, 0, sample_n, sample_n)
+        tl = time.perf_counter() - t3
+        epoch = ITERS * (tg * w["s"] / sample_n + ta) + tl * w["f"] / sample_n
+        if s >= warmup:
+            times.append((epoch, tg + ta + tl))
+    ep = float(np.median([e for e, _ in times]))
+    return dict(epoch_s=ep, wall_per_step=float(np.mean([x for _, x in times])), setup_s=setup)
+
+
+def reference_arm(args, ws, rank):
+    if rank != 0:
+        return
+    name = args.config
+    w = workload(name)
+    subs, vals, _ = make_tensor(name, "cuda" if torch.cuda.is_available() else "cpu")
+    subs_h, vals_h = subs.cpu().numpy(), vals.cpu().numpy()
+    del subs, vals
+    n = args.cpu_sample
+    r = run_oracle_sample(name, subs_h, vals_h, args.steps, args.warmup, n)
+    eps = 1.0 / r["epoch_s"]
+    sample = (f"oracle (fp64, 1 thread) per step: 1 sampled gradient with p'=q'={n}, 1 Adam pass over all "
+              f"{sum(w['dims']) * w['R']} coefficients, 1 loss estimate with f'={n}; extrapolated to one epoch "
+              f"(100 iterations at p=q={w['s']:.0e}, f={w['f']:.0e})")
+    line = {"impl": "reference", "metric": METRIC, "value": eps, "unit": "epochs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["epoch_s"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{name}: {w['desc']}", "parallelism": "cpu-1thread"},
+            "samples_per_s": eps * ITERS * 2 * w["s"],
+            "cpu_baseline": {"value": eps, "unit": "epochs/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": eps, "unit": "epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--mode", default="sync", choices=["sync", "async", "fedadam"])
+    ap.add_argument("--tau", type=int, default=10)
+    ap.add_argument("--cpu-sample", type=int, default=100_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("GCP_BENCH_ALLOW_SHORT"), "W >= 3"
+
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        reference_arm(args, ws, rank)
+        return
+
+    import paper_2605_20353_b200 as g
+
+    name = args.config
+    w = workload(name)
+    dev = local
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = g.Context(dev, stream.cuda_stream, args.precision)
+    uid = bcast_bytes(ws, rank, g.gcp_nccl_unique_id() if (rank == 0 and ws > 1) else None)
+    ctx.dist_init(ws, rank, uid, None, args.mode)
+    grid, lo, hi = g.gcp_grid_plan(ws, w["dims"])
+
+    subs, vals, gen_s = make_tensor(name, f"cuda:{dev}")
+    bs, bv = block_of(subs, vals, lo[rank], hi[rank])
+    del subs, vals
+    subs_h = bs.cpu().pin_memory()
+    vals_h = bv.cpu().pin_memory()
+    nnz_local = len(vals_h)
+    del bs, bv
+    torch.cuda.empty_cache()
+    t0 = time.time()
+    ctx.tensor_create_ptr(w["dims"], nnz_local, subs_h.data_ptr(), vals_h.data_ptr())
+    ingest_s = time.time() - t0
+    ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
+    fp = ctx.fit_params(epochs=10 ** 6, iters_per_epoch=ITERS, max_fails=10 ** 6, s_nz=w["s"], s_z=w["s"],
+                        f_nz=w["f"], f_z=w["f"], loss=w["loss"], seed=gcp_synth.SEEDS[name]["sample"], fseed=2,
+                        rate=1e-3, tau=args.tau if args.mode != "sync" else 0, meta_rate=1e-3)
+    ctx.fit_begin(fp)
+    for _ in range(args.warmup):
+        ctx.fit_epoch()
+    ctx.profile_enable(True)
+    for k in g.gcp.PROF:
+        ctx.profile_get(k, reset=True)
+    c0 = ctx.counters()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.fit_epoch()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms_local = ev0.elapsed_time(ev1)
+    ms = allmax(ws, ms_local)
+    c1 = ctx.counters()
+    prof = {k: ctx.profile_get(k) for k in g.gcp.PROF}
+    ctx.profile_enable(False)
+    ms_step = ms / args.steps
+    eps = 1000.0 / ms_step
+    samples_per_s = eps * ITERS * (2 * w["s"])
+    launches = sum(prof[k][1] for k in ("grad", "adam", "loss", "other"))
+    # ---- roofline of the dominant kernel (K2, fused sampling-MTTKRP)
+    k2_ms, k2_n = prof["grad"]
+    p_loc = w["s"] // ws + (1 if rank < w["s"] % ws else 0)
+    alg_bytes = p_loc * w["nz_bytes"] + p_loc * w["z_bytes"]
+    k2_avg_ms = allmax(ws, k2_ms / max(k2_n, 1))
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (k2_avg_ms * 1e-3) / 1e9
+    traffic = None
+    tr = ROOT / "profiles" / f"ncu_traffic_{name}.json"
+    if tr.exists():
+        traffic = json.loads(tr.read_text()).get("k2_dram_bytes_per_launch")
+    # ---- e2e: the public API from pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(g, ctx, w, name, fp, subs_h, vals_h, dev, stream, ws, args)
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = run_oracle_sample(name, subs_h.numpy(), vals_h.numpy(), 2, 1, args.cpu_sample)
+        cpu = {"value": 1.0 / r["epoch_s"], "unit": "epochs/s", "cores": 1, "kind": "oracle",
+               "sample": (f"1 sampled gradient (p'=q'={args.cpu_sample}) + 1 Adam pass + 1 loss estimate "
+                          f"(f'={args.cpu_sample}) per step, median of 2 steps after 1 warm-up, extrapolated to "
+                          f"one epoch of 100 iterations at p=q={w['s']:.0e}; fp64 single-thread C oracle")}
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": eps, "unit": "epochs/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{name}: {w['desc']}", "dims": list(w["dims"]), "nnz": int(w["nnz"]),
+                       "R": w["R"], "loss": w["loss"], "p": w["s"], "q": w["s"], "f_nz": w["f"], "f_z": w["f"],
+                       "iters_per_epoch": ITERS, "grid": list(grid), "dist_mode": args.mode,
+                       "parallelism": f"grid{'x'.join(map(str, grid))}-{args.mode}" if ws > 1 else "single-gpu",
+                       "l2": "inputs larger than L2 (COO records + hash set >> 126 MB); factors stay L2-resident",
+                       "nnz_local_rank0": nnz_local},
+            "samples_per_s": samples_per_s,
+            "hbm_gbs_k2_algorithmic": achieved,
+            "gpu_launches": int(launches),
+            "library_launches_total": int(c1["launches"] - c0["launches"]),
+            "phase_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_sample (K2 fused sampling-MTTKRP)",
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k2_avg_ms, "peak_source": peak_src},
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "setup_s": {"generate": gen_s, "ingest": ingest_s},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_e2e(g, ctx, w, name, fp, subs_h, vals_h, dev, stream, ws, args):
+    """Per step: ingest the COO from pinned host memory (H2D), upload the initial
+    factors from host (H2D), fit_begin + one epoch, read back the factors and the
+    loss (D2H) -- the job a user runs through the public API."""
+    A0 = [ctx.model_get(k) for k in range(w["d"])]
+    h2d = subs_h.numel() * 8 + vals_h.numel() * 8 + sum(a.size * 8 for a in A0)
+    d2h = sum(a.size * 8 for a in A0) + 8
+    steps = max(1, min(args.steps, 3))
+    times = []
+    for s in range(steps + 1):
+        barrier(ws)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.tensor_create_ptr(w["dims"], vals_h.numel(), subs_h.data_ptr(), vals_h.data_ptr())
+        ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
+        for k in range(w["d"]):
+            ctx.model_set(k, A0[k])
+        ctx.fit_begin(fp)
+        est, _, _ = ctx.fit_epoch()
+        _ = [ctx.model_get(k) for k in range(w["d"])]
+        torch.cuda.synchronize()
+        dt = allmax(ws, time.perf_counter() - t0)
+        if s > 0:
+            times.append(dt)
+    t = float(np.median(times))
+    return {"value": 1.0 / t, "unit": "epochs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": t * 1e3, "steps": steps,
+            "includes": "H2D COO + ingest (sort, dup check, hash) + H2D factors + F0 estimate + 1 epoch + D2H"}
+
+
+if __name__ == "__main__":
+    main()

@@ -285,6 +285,13 @@ gcp_status gcp_create(gcp_ctx** out, int cuda_device, void* cuda_stream, gcp_pre
     if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess)
         return set_error(GCP_E_CUDA, "gcp_create: cudaGetDeviceProperties failed");
     if (prop.major != 10) return set_error(GCP_E_CUDA, "gcp_create: libgcp is built for sm_100a (B200) only");
+    // Random 16-32 B record / bucket reads: ask L2 not to widen DRAM fetches
+    // (device-wide hint; GCP_L2_FETCH overrides, 0 leaves the driver default).
+    {
+        const char* env = getenv("GCP_L2_FETCH");
+        const long v = env ? strtol(env, nullptr, 10) : 32;
+        if (v > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)v);
+    }
     gcp_ctx* c = new gcp_ctx();
     c->dev = cuda_device;
     c->stream = (cudaStream_t)cuda_stream;

@@ -117,70 +117,154 @@ template <> __device__ __forceinline__ double load_val<double>(const uint32_t* r
     return __hiloint2double((int)r[1], (int)r[0]);
 }
 
-// Draw the sample of local slot `s` (0 <= s < p: nonzero slot s; p <= s < p+q:
-// zero slot s-p).  Pure function of (seed, rank, kind, it, slot) and the tensor.
-template <typename T, int D>
-__device__ __forceinline__ Sample<T, D> draw_sample(const SampleArgs& a, int64_t s) {
-    Sample<T, D> o;
+// A sample whose one dependent DRAM access (the COO record of a nonzero slot,
+// or the first hash bucket of a zero candidate) has been issued but not yet
+// consumed.  Splitting draw into issue + resolve lets the kernel keep the next
+// chunk's random DRAM reads in flight while it works on the current chunk.
+template <int D>
+struct Pending {
+    uint4 w0, w1;        // record words / bucket words as loaded
+    uint32_t c[D];       // zero candidate (attempt 0)
+    uint32_t slot;       // local slot within the stratum
+    int state;           // 0 invalid, 1 nonzero, 2 zero (probe pending), 3 zero (no probe)
+    uint32_t j;          // nonzero index (low 32 bits; high bits recomputed if N >= 2^32)
+};
+
+template <int D>
+__device__ __forceinline__ void zero_candidate(const SampleArgs& a, uint32_t zs, uint32_t att, uint32_t (&c)[D]) {
     const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+#pragma unroll
+    for (int g = 0; g < (D + 1) / 2; ++g) {
+        const U64x2 w = philox(zs, a.rank, (a.kind_z << 28) | (att << 4) | (uint32_t)g, a.it, k0, k1);
+        c[2 * g] = (uint32_t)range_map(w.w0, a.bdim[2 * g]);
+        if (2 * g + 1 < D) c[2 * g + 1] = (uint32_t)range_map(w.w1, a.bdim[2 * g + 1]);
+    }
+}
+
+// first bucket (32 B) of the probe sequence of candidate c, as a word offset into the table
+template <int D>
+__device__ __forceinline__ uint64_t first_bucket(const SampleArgs& a, const uint32_t (&c)[D], uint64_t& klo,
+                                                 uint64_t& khi) {
+    if (!a.key128) {
+        uint64_t key = c[0];
+#pragma unroll
+        for (int k = 1; k < D; ++k) key = key * a.bdim[k] + c[k];
+        klo = key;
+        khi = 0;
+        return (hash_key(key, 0) & a.hash_mask) & ~3ull;
+    }
+    unsigned __int128 key = c[0];
+#pragma unroll
+    for (int k = 1; k < D; ++k) key = key * a.bdim[k] + c[k];
+    klo = (uint64_t)key;
+    khi = (uint64_t)(key >> 64);
+    return 2 * ((hash_key(klo, khi) & a.hash_mask) & ~1ull);
+}
+
+template <typename T, int D>
+__device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t s) {
+    Pending<D> P;
+    P.state = 0;
+    if (s >= a.p + a.q) return P;
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    constexpr int VW = (int)(sizeof(T) / 4);
     if (s < a.p) {
         // nonzero slot: j uniform over [0, N) with replacement
         const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, a.it, k0, k1);
-        const int64_t j = (int64_t)range_map(w.w0, (uint64_t)a.N);
-        const uint32_t* r = a.rec + j * a.rec_words;
-        constexpr int VW = (int)(sizeof(T) / 4);   // value words at the record head
-        if (VW + D <= 4) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(r));
-            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-            o.x = load_val<T>(w4);
+        const uint64_t j = range_map(w.w0, (uint64_t)a.N);
+        const uint4* r = reinterpret_cast<const uint4*>(a.rec + j * a.rec_words);
+        P.w0 = __ldg(r);
+        if (VW + D > 4) P.w1 = __ldg(r + 1);
+        P.slot = (uint32_t)s;
+        P.j = (uint32_t)j;
+        P.state = 1;
+        return P;
+    }
+    // zero slot, attempt 0: draw d indices and issue the first probe
+    P.slot = (uint32_t)(s - a.p);
+    zero_candidate<D>(a, P.slot, 0u, P.c);
+    if (!a.stratified) {
+        P.state = 3;
+        return P;
+    }
+    uint64_t klo, khi;
+    const uint64_t b = first_bucket<D>(a, P.c, klo, khi);
+    const uint4* h = reinterpret_cast<const uint4*>(a.hash + b);
+    P.w0 = __ldg(h);
+    P.w1 = __ldg(h + 1);
+    P.state = 2;
+    return P;
+}
+
+// 0 absent, 1 present, 2 undecided (bucket full of other keys: continue probing)
+__device__ __forceinline__ int bucket_verdict(const SampleArgs& a, const uint4& w0, const uint4& w1, uint64_t klo,
+                                              uint64_t khi) {
+    const uint64_t s0 = ((uint64_t)w0.y << 32) | w0.x, s1 = ((uint64_t)w0.w << 32) | w0.z;
+    const uint64_t s2 = ((uint64_t)w1.y << 32) | w1.x, s3 = ((uint64_t)w1.w << 32) | w1.z;
+    if (!a.key128) {
+        if (s0 == klo || s1 == klo || s2 == klo || s3 == klo) return 1;
+        if (s0 == kEmpty || s1 == kEmpty || s2 == kEmpty || s3 == kEmpty) return 0;
+        return 2;
+    }
+    if ((s0 == klo && s1 == khi) || (s2 == klo && s3 == khi)) return 1;
+    if ((s0 == kEmpty && s1 == kEmpty) || (s2 == kEmpty && s3 == kEmpty)) return 0;
+    return 2;
+}
+
+__device__ __forceinline__ bool probe_from(const SampleArgs& a, uint64_t klo, uint64_t khi) {
+    return a.key128 ? set_contains128(a.hash, a.hash_mask, klo, khi) : set_contains64(a.hash, a.hash_mask, klo);
+}
+
+template <typename T, int D>
+__device__ __forceinline__ Sample<T, D> resolve_sample(const SampleArgs& a, const Pending<D>& P) {
+    Sample<T, D> o;
+    constexpr int VW = (int)(sizeof(T) / 4);
+    if (P.state == 1) {
+        const uint32_t w8[8] = {P.w0.x, P.w0.y, P.w0.z, P.w0.w, P.w1.x, P.w1.y, P.w1.z, P.w1.w};
+        o.x = load_val<T>(w8);
 #pragma unroll
-            for (int k = 0; k < D; ++k) o.c[k] = w4[(VW + k) & 3];
-        } else {
-            const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(r));
-            const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(r) + 1);
-            const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-            o.x = load_val<T>(w8);
-#pragma unroll
-            for (int k = 0; k < D; ++k) o.c[k] = w8[(VW + k) & 7];
+        for (int k = 0; k < D; ++k) o.c[k] = w8[(VW + k) & 7];
+        uint64_t j = P.j;
+        if ((uint64_t)a.N > 0xFFFFFFFFull) {
+            const U64x2 w = philox(P.slot, a.rank, a.kind_nz << 28, a.it, (uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+            j = range_map(w.w0, (uint64_t)a.N);
         }
-        o.j = j;
+        o.j = (int64_t)j;
         o.attempts = 1;
         o.nz = true;
         return o;
     }
-    // zero slot: draw d indices, reject while the candidate is a nonzero
-    const uint32_t zs = (uint32_t)(s - a.p);
     o.x = T(0);
     o.j = -1;
     o.nz = false;
-    for (uint32_t att = 0;; ++att) {
+    o.attempts = 1;
 #pragma unroll
-        for (int g = 0; g < (D + 1) / 2; ++g) {
-            const U64x2 w = philox(zs, a.rank, (a.kind_z << 28) | (att << 4) | (uint32_t)g, a.it, k0, k1);
-            o.c[2 * g] = (uint32_t)range_map(w.w0, a.bdim[2 * g]);
-            if (2 * g + 1 < D) o.c[2 * g + 1] = (uint32_t)range_map(w.w1, a.bdim[2 * g + 1]);
-        }
-        o.attempts = (int)att + 1;
-        if (!a.stratified) break;
-        bool present;
-        if (!a.key128) {
-            uint64_t key = o.c[0];
-#pragma unroll
-            for (int k = 1; k < D; ++k) key = key * a.bdim[k] + o.c[k];
-            present = set_contains64(a.hash, a.hash_mask, key);
-        } else {
-            unsigned __int128 key = o.c[0];
-#pragma unroll
-            for (int k = 1; k < D; ++k) key = key * a.bdim[k] + o.c[k];
-            present = set_contains128(a.hash, a.hash_mask, (uint64_t)key, (uint64_t)(key >> 64));
-        }
-        if (!present) break;
-        if (att + 1 >= (uint32_t)kRejectCap) {
-            atomicMin(a.err_slot, (unsigned long long)zs);
+    for (int k = 0; k < D; ++k) o.c[k] = P.c[k];
+    if (P.state != 2) return o;
+    // zero candidate: decide attempt 0 from the prefetched bucket; rejected
+    // candidates redraw all d indices -- rare, handled inline
+    uint64_t klo, khi;
+    first_bucket<D>(a, o.c, klo, khi);
+    int v = bucket_verdict(a, P.w0, P.w1, klo, khi);
+    bool present = v == 1 || (v == 2 && probe_from(a, klo, khi));
+    for (uint32_t att = 1; present; ++att) {
+        if (att >= (uint32_t)kRejectCap) {
+            atomicMin(a.err_slot, (unsigned long long)P.slot);
             break;
         }
+        zero_candidate<D>(a, P.slot, att, o.c);
+        o.attempts = (int)att + 1;
+        first_bucket<D>(a, o.c, klo, khi);
+        present = probe_from(a, klo, khi);
     }
     return o;
+}
+
+// Draw the sample of local slot `s` (0 <= s < p: nonzero slot s; p <= s < p+q:
+// zero slot s-p).  Pure function of (seed, rank, kind, it, slot) and the tensor.
+template <typename T, int D>
+__device__ __forceinline__ Sample<T, D> draw_sample(const SampleArgs& a, int64_t s) {
+    return resolve_sample<T, D>(a, issue_sample<T, D>(a, s));
 }
 
 }  // namespace gcp

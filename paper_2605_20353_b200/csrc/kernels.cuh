@@ -94,11 +94,16 @@ __global__ void __launch_bounds__(kBlock, kSampleMinBlocks) k_sample(const Sampl
     }
 
     double lacc = 0.0;
+    // software pipeline: the next chunk's record / first-bucket loads are in
+    // flight while this chunk's rows are gathered and scattered
+    Pending<D> nxt = issue_sample<T, D>(sa, (warp0 << 5) + lane);
     for (int64_t chunk = warp0; chunk < nchunks; chunk += nwarps) {
         const int64_t s = (chunk << 5) + lane;
         const bool valid = s < total;
+        const Pending<D> cur = nxt;
+        nxt = issue_sample<T, D>(sa, ((chunk + nwarps) << 5) + lane);
         Sample<T, D> smp;
-        if (valid) smp = draw_sample<T, D>(sa, s);
+        if (valid) smp = resolve_sample<T, D>(sa, cur);
         else {
 #pragma unroll
             for (int k = 0; k < D; ++k) smp.c[k] = 0;

@@ -1,0 +1,64 @@
+"""Per-kernel timing of the hot path on one config (development tool).
+
+    python tools/k2bench.py [--config c2] [--iters 20]
+
+Times K2 (fused sampling-MTTKRP), K3 (Adam) and the loss estimate separately
+with the library's CUDA-event profiler; prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import gcp_synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--precision", default="fp32")
+    args = ap.parse_args()
+    import paper_2605_20353_b200 as g
+    c = gcp_synth.CONFIGS[args.config]
+    s = gcp_synth.SEEDS[args.config]
+    subs, vals = gcp_synth.chi_kolda(c["dims"], c["nnz"], c["R"], s["data"], c["loss"], device="cuda")
+    subs_h, vals_h = subs.cpu().pin_memory(), vals.cpu().pin_memory()
+    del subs, vals
+    torch.cuda.empty_cache()
+    stream = torch.cuda.Stream()
+    ctx = g.Context(0, stream.cuda_stream, args.precision)
+    t0 = time.time()
+    ctx.tensor_create_ptr(c["dims"], vals_h.numel(), subs_h.data_ptr(), vals_h.data_ptr())
+    t_ingest = time.time() - t0
+    ctx.model_init(c["R"], s["model"])
+    ctx.sample("stratified", c["s"], c["s"], s["sample"])
+    for _ in range(3):
+        ctx.loss_grad(c["loss"])
+        ctx.adam_step()
+    ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
+    ctx.profile_enable(True)
+    for k in ("grad", "adam", "loss", "other"):
+        ctx.profile_get(k, reset=True)
+    for _ in range(args.iters):
+        ctx.loss_grad(c["loss"])
+        ctx.adam_step()
+    for _ in range(3):
+        ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
+    out = {"config": args.config, "L2_FETCH": os.environ.get("GCP_L2_FETCH", "default(32)"), "ingest_s": t_ingest}
+    for k in ("grad", "adam", "loss"):
+        ms, n = ctx.profile_get(k)
+        out[k + "_ms"] = ms / max(n, 1)
+    out["samples_per_s_k2"] = 2 * c["s"] / (out["grad_ms"] * 1e-3)
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

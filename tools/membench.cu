@@ -1,0 +1,128 @@
+// membench.cu -- random-access ceilings of the B200 memory system for the access
+// patterns of the GCP hot path (development tool; not part of libgcp.so).
+//
+//   rand16_hbm : random 16-B loads from a 2 GiB array (COO record fetch pattern)
+//   rand32_hbm : random 32-B loads (two 16-B halves of one sector; hash bucket)
+//   rand64_l2  : random 64-B rows (4 lanes x 16 B) from a 2 MiB array (L2-resident factors)
+//   red64_l2   : random 64-B vector red.add rows into a 2 MiB array (gradient scatter)
+//   copy_hbm   : streaming float4 copy (reference)
+//
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/membench tools/membench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint64_t mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <int ILP>
+__global__ void rand_load(const uint4* __restrict__ a, uint64_t n, int64_t total, int words, uint32_t* sink) {
+    uint32_t acc = 0;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < total; i += nt * ILP) {
+        uint4 v[ILP], u[ILP];
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) {
+            const uint64_t j = __umul64hi(mix(i + k * nt), n);
+            v[k] = __ldg(a + j * words);
+            if (words == 2) u[k] = __ldg(a + j * words + 1);
+        }
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) {
+            acc += v[k].x ^ v[k].w;
+            if (words == 2) acc += u[k].y;
+        }
+    }
+    if (acc == 0x12345678u) *sink = acc;
+}
+
+// groups of 4 lanes read one 64-B row each
+template <int ILP>
+__global__ void rand_rows(const float4* __restrict__ a, uint64_t rows, int64_t total, float* sink) {
+    float acc = 0.f;
+    const int lane = threadIdx.x & 3;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 2;
+    for (int64_t i = g; i < total; i += ng * ILP) {
+        float4 v[ILP];
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) {
+            const uint64_t r = __umul64hi(mix(i + k * ng), rows);
+            v[k] = __ldg(a + r * 4 + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) acc += v[k].x + v[k].w;
+    }
+    if (acc == 1.2345f) *sink = acc;
+}
+
+__global__ void rand_red(float4* a, uint64_t rows, int64_t total) {
+    const int lane = threadIdx.x & 3;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 2;
+    for (int64_t i = g; i < total; i += ng) {
+        const uint64_t r = __umul64hi(mix(i), rows);
+        float* p = reinterpret_cast<float*>(a + r * 4 + lane);
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.f), "f"(1.f), "f"(1.f), "f"(1.f)
+                     : "memory");
+    }
+}
+
+__global__ void copy4(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+template <typename F>
+static float timeit(F f, int reps = 5) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    f();
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms / reps;
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const size_t big = 2ull << 30, small = 2ull << 20;
+    uint4* A;
+    float4 *S, *B;
+    uint32_t* sink;
+    cudaMalloc(&A, big);
+    cudaMalloc(&B, big);
+    cudaMalloc(&S, small);
+    cudaMalloc(&sink, 64);
+    cudaMemset(A, 1, big);
+    cudaMemset(S, 0, small);
+    const int64_t total = 1ll << 26;
+    printf("{");
+    for (int blocks : {sms * 4, sms * 8, sms * 16}) {
+        float ms = timeit([&] { rand_load<4><<<blocks, 256>>>(A, big / 16, total, 1, sink); });
+        printf("\"rand16_hbm_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_load<4><<<blocks, 256>>>(A, big / 32, total, 2, sink); });
+        printf("\"rand32_hbm_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_load<1><<<blocks, 256>>>(A, big / 16, total, 1, sink); });
+        printf("\"rand16_hbm_ilp1_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_rows<4><<<blocks, 256>>>(S, small / 64, total, (float*)sink); });
+        printf("\"rand64_l2_rows_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_red<<<blocks, 256>>>(S, small / 64, total); });
+        printf("\"red64_l2_rows_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+    }
+    const int64_t n4 = big / 16;
+    float ms = timeit([&] { copy4<<<sms * 8, 256>>>((const float4*)A, B, n4); });
+    printf("\"copy_hbm_GBps\": %.1f}\n", 2.0 * big / (ms * 1e-3) / 1e9);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+    return 0;
+}
