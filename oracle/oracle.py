@@ -363,6 +363,14 @@ def split_blocks(dims, subs, vals, P, grid=None):
     return blocks, grid
 
 
+def local_counts(t, total_nz, total_z, P, w, stratified=True):
+    """Per-rank sample counts (reading R13) with the empty-strata rule of
+    SURVEY §8(c) C4: a block without nonzeros (zeros) draws none of them."""
+    p = alloc_count(total_nz, P, w) if t.nnz > 0 else 0
+    q = alloc_count(total_z, P, w) if t.M > t.nnz else 0
+    return p, q
+
+
 def sync_gradient(blocks, A, loss, seed, it, p, q, strategy="stratified", lam=None):
     """Alg. 2 lines 2-3: each rank's sampled gradient, summed into the global
     G^(k) in rank-major order.  Returns (G, S, sampled loss)."""
@@ -371,8 +379,8 @@ def sync_gradient(blocks, A, loss, seed, it, p, q, strategy="stratified", lam=No
     S = [np.zeros_like(a, dtype=np.float64) for a in A]
     ls = 0.0
     for w, t in enumerate(blocks):
-        Gw, Sw, lw = sampled_grad(t, A, loss, seed, w, it, alloc_count(p, P, w),
-                                  alloc_count(q, P, w), strategy, lam)
+        pw, qw = local_counts(t, p, q, P, w)
+        Gw, Sw, lw = sampled_grad(t, A, loss, seed, w, it, pw, qw, strategy, lam)
         for k in range(t.d):
             G[k][t.lo[k]:t.hi[k]] += Gw[k]
             S[k][t.lo[k]:t.hi[k]] += Sw[k]
@@ -386,8 +394,8 @@ def sync_loss_estimate(blocks, A_of_rank, loss, seed, f_nz, f_z, lam=None):
     P = len(blocks)
     est = sc = 0.0
     for w, t in enumerate(blocks):
-        e, s = loss_estimate(t, A_of_rank(w), loss, seed, w, alloc_count(f_nz, P, w),
-                             alloc_count(f_z, P, w), lam)
+        fn, fz = local_counts(t, f_nz, f_z, P, w)
+        e, s = loss_estimate(t, A_of_rank(w), loss, seed, w, fn, fz, lam)
         est += e
         sc += s
     return est, sc
@@ -402,99 +410,125 @@ def slice_groups(grid, k):
     return [groups[b] for b in sorted(groups)]
 
 
+class MultiRank:
+    """State of a P-rank run and one iteration of Alg. 2 (sync), Alg. 3
+    (LocalSGD, reading R16) or Alg. 4 (FedAdam, reading R17), with the
+    iteration counter semantics of reading R18."""
+
+    def __init__(self, blocks, grid, A0, loss, mode="sync", beta1=0.9, beta2=0.999, eps=1e-8,
+                 lower=None, strategy="stratified", tau=1, meta_rate=1e-3, lam=None):
+        self.blocks, self.grid, self.loss, self.mode = blocks, grid, loss, mode
+        self.P, self.d = len(blocks), len(A0)
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.lower = loss_lower(loss) if lower is None else lower
+        self.strategy, self.tau, self.meta_rate, self.lam = strategy, tau, meta_rate, lam
+        self.R = A0[0].shape[1]
+        self.dims = [a.shape[0] for a in A0]
+        if mode == "sync":
+            self.st = {"A": [np.array(a, np.float64) for a in A0],
+                       "B": [np.zeros_like(a, np.float64) for a in A0],
+                       "C": [np.zeros_like(a, np.float64) for a in A0], "t": 0}
+        else:
+            st = {"A": [], "B": [], "C": [], "t": [0] * self.P, "U": [], "Bs": [], "Cs": [], "ts": [0] * self.P}
+            for w, tb in enumerate(blocks):
+                Aw = [np.array(A0[k][tb.lo[k]:tb.hi[k]], np.float64) for k in range(self.d)]
+                st["A"].append(Aw)
+                st["B"].append([np.zeros_like(a) for a in Aw])
+                st["C"].append([np.zeros_like(a) for a in Aw])
+                st["U"].append([a.copy() for a in Aw])
+                st["Bs"].append([np.zeros_like(a) for a in Aw])
+                st["Cs"].append([np.zeros_like(a) for a in Aw])
+            self.st = st
+
+    def model_for_rank(self, w):
+        """Global-shaped factors as rank w sees them (its replica in async modes)."""
+        if self.mode == "sync":
+            return self.st["A"]
+        tb = self.blocks[w]
+        full = [np.zeros((self.dims[k], self.R)) for k in range(self.d)]
+        for k in range(self.d):
+            full[k][tb.lo[k]:tb.hi[k]] = self.st["A"][w][k]
+        return full
+
+    def block_rows(self, w, k):
+        tb = self.blocks[w]
+        if self.mode == "sync":
+            return self.st["A"][k][tb.lo[k]:tb.hi[k]]
+        return self.st["A"][w][k]
+
+    def _adam_list(self, As, Gs, Bs, Cs, t, rate):
+        for k in range(self.d):
+            adam(As[k].reshape(-1), np.ascontiguousarray(Gs[k], np.float64).reshape(-1),
+                 Bs[k].reshape(-1), Cs[k].reshape(-1), t, rate, self.beta1, self.beta2, self.eps, self.lower)
+
+    def async_sync(self):
+        """Alg. 3 lines 2-4 / Alg. 4 lines 3-6 over every mode's slice groups."""
+        st = self.st
+        for k in range(self.d):
+            for grp in slice_groups(self.grid, k):
+                if self.mode == "async":      # average over the g_k replicas
+                    avg = sum(st["A"][w][k] for w in grp) / len(grp)
+                    for w in grp:
+                        st["A"][w][k][...] = avg
+                else:                         # D = U - M, AllReduce(D) (sum), server Adam on U, M <- U
+                    S = sum(st["U"][w][k] - st["A"][w][k] for w in grp)
+                    for w in grp:
+                        adam(st["U"][w][k].reshape(-1), np.ascontiguousarray(S, np.float64).reshape(-1),
+                             st["Bs"][w][k].reshape(-1), st["Cs"][w][k].reshape(-1), st["ts"][w] + 1,
+                             self.meta_rate, self.beta1, self.beta2, self.eps, self.lower)
+                        st["A"][w][k][...] = st["U"][w][k]
+        if self.mode == "fedadam":
+            for w in range(self.P):
+                st["ts"][w] += 1
+
+    def iteration(self, it, seed, s_nz, s_z, rate):
+        """One mini-batch iteration with Philox iteration word `it`."""
+        st = self.st
+        if self.mode == "sync":
+            G, _, _ = sync_gradient(self.blocks, st["A"], self.loss, seed, it, s_nz, s_z, self.strategy, self.lam)
+            st["t"] += 1
+            self._adam_list(st["A"], G, st["B"], st["C"], st["t"], rate)
+            return
+        if (it + 1) % self.tau == 0:
+            self.async_sync()
+        for w, tb in enumerate(self.blocks):
+            pw, qw = local_counts(tb, s_nz, s_z, self.P, w)
+            Gw, _, _ = sampled_grad(tb, self.model_for_rank(w), self.loss, seed, w, it, pw, qw,
+                                    self.strategy, self.lam, with_scale=False)
+            st["t"][w] += 1
+            self._adam_list(st["A"][w], Gw, st["B"][w], st["C"][w], st["t"][w], rate)
+
+    def estimate(self, fseed, f_nz, f_z):
+        return sync_loss_estimate(self.blocks, self.model_for_rank, self.loss, fseed, f_nz, f_z, self.lam)
+
+
 def fit(blocks, grid, A0, loss, *, epochs=10, iters=100, max_fails=3, rate=1e-3, decay=0.1,
         beta1=0.9, beta2=0.999, eps=1e-8, lower=None, s_nz=1000, s_z=1000, f_nz=1000,
         f_z=1000, seed=1, fseed=2, strategy="stratified", mode="sync", tau=1,
         meta_rate=None, lam=None, trace=None):
     """Epoch loop with annealing (reading R20) around Alg. 2 / 3 / 4.
 
-    Returns (final global A, list of per-epoch (est_loss, rate, accepted))."""
-    P = len(blocks)
-    d = len(A0)
-    if lower is None:
-        lower = loss_lower(loss)
-    if meta_rate is None:
-        meta_rate = rate
-    # per-rank replicas (async modes) or one global model (sync)
-    if mode == "sync":
-        st = {"A": [np.array(a, np.float64) for a in A0],
-              "B": [np.zeros_like(a, np.float64) for a in A0],
-              "C": [np.zeros_like(a, np.float64) for a in A0], "t": 0}
-    else:
-        st = {"A": [], "B": [], "C": [], "t": [0] * P, "U": [], "Bs": [], "Cs": [], "ts": [0] * P}
-        for w, tb in enumerate(blocks):
-            Aw = [np.array(A0[k][tb.lo[k]:tb.hi[k]], np.float64) for k in range(d)]
-            st["A"].append(Aw)
-            st["B"].append([np.zeros_like(a) for a in Aw])
-            st["C"].append([np.zeros_like(a) for a in Aw])
-            st["U"].append([a.copy() for a in Aw])
-            st["Bs"].append([np.zeros_like(a) for a in Aw])
-            st["Cs"].append([np.zeros_like(a) for a in Aw])
-
-    def model_for_rank(w):
-        if mode == "sync":
-            return st["A"]
-        tb = blocks[w]
-        full = [np.zeros((tb.dims[k], A0[k].shape[1])) for k in range(d)]
-        for k in range(d):
-            full[k][tb.lo[k]:tb.hi[k]] = st["A"][w][k]
-        return full
-
-    def adam_list(As, Gs, Bs, Cs, t, a):
-        for k in range(d):
-            Af, Gf = As[k].reshape(-1), np.ascontiguousarray(Gs[k], np.float64).reshape(-1)
-            Bf, Cf = Bs[k].reshape(-1), Cs[k].reshape(-1)
-            adam(Af, Gf, Bf, Cf, t, a, beta1, beta2, eps, lower)
-
-    def estimate():
-        return sync_loss_estimate(blocks, model_for_rank, loss, fseed, f_nz, f_z, lam)[0]
-
+    Returns (final factors (global list for sync, per-rank global-shaped lists
+    otherwise), list of per-epoch (est_loss, rate, accepted), best estimate)."""
     import copy
-    best = estimate()
-    ckpt = copy.deepcopy(st)
+    run = MultiRank(blocks, grid, A0, loss, mode, beta1, beta2, eps, lower, strategy, tau,
+                    rate if meta_rate is None else meta_rate, lam)
+    best = run.estimate(fseed, f_nz, f_z)[0]
+    ckpt = copy.deepcopy(run.st)
     it = 0
     fails = 0
     hist = []
     for e in range(epochs):
         for _ in range(iters):
-            if mode == "sync":
-                G, _, _ = sync_gradient(blocks, st["A"], loss, seed, it, s_nz, s_z, strategy, lam)
-                st["t"] += 1
-                adam_list(st["A"], G, st["B"], st["C"], st["t"], rate)
-            else:
-                t_it = it + 1
-                if t_it % tau == 0:
-                    for k in range(d):
-                        for grp in slice_groups(grid, k):
-                            if mode == "async":      # Alg. 3: average over the g_k replicas
-                                avg = sum(st["A"][w][k] for w in grp) / len(grp)
-                                for w in grp:
-                                    st["A"][w][k][...] = avg
-                            else:                    # Alg. 4: D = U - M, sum, server Adam on U
-                                S = sum(st["U"][w][k] - st["A"][w][k] for w in grp)
-                                for w in grp:
-                                    Uk = st["U"][w][k].reshape(-1)
-                                    adam(Uk, np.ascontiguousarray(S, np.float64).reshape(-1),
-                                         st["Bs"][w][k].reshape(-1), st["Cs"][w][k].reshape(-1),
-                                         st["ts"][w] + 1, meta_rate, beta1, beta2, eps, lower)
-                                    st["A"][w][k][...] = st["U"][w][k]
-                    if mode == "fedadam":
-                        for w in range(P):
-                            st["ts"][w] += 1
-                for w, tb in enumerate(blocks):
-                    Gw, _, _ = sampled_grad(tb, model_for_rank(w), loss, seed, w, it,
-                                            alloc_count(s_nz, P, w), alloc_count(s_z, P, w),
-                                            strategy, lam, with_scale=False)
-                    st["t"][w] += 1
-                    adam_list(st["A"][w], Gw, st["B"][w], st["C"][w], st["t"][w], rate)
+            run.iteration(it, seed, s_nz, s_z, rate)
             it += 1
-        est = estimate()
+        est = run.estimate(fseed, f_nz, f_z)[0]
         if est < best:
             best = est
-            ckpt = copy.deepcopy(st)
+            ckpt = copy.deepcopy(run.st)
             hist.append((est, rate, True))
         else:
-            st = copy.deepcopy(ckpt)
+            run.st = copy.deepcopy(ckpt)
             hist.append((est, rate, False))
             rate *= decay
             fails += 1
@@ -503,5 +537,5 @@ def fit(blocks, grid, A0, loss, *, epochs=10, iters=100, max_fails=3, rate=1e-3,
         if fails >= max_fails:
             break
     if mode == "sync":
-        return st["A"], hist, best
-    return [model_for_rank(w) for w in range(P)], hist, best
+        return run.st["A"], hist, best
+    return [run.model_for_rank(w) for w in range(len(blocks))], hist, best

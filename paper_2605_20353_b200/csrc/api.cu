@@ -547,7 +547,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     ST_TRY(ensure_partials(c, c->grad_blocks));
     c->have_model = true;
     c->have_grad = false;
-    return GCP_OK;
+    return server_reset(c);   // FedAdam: U <- M0 (Alg. 4)
 }
 
 gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* lambda) {
@@ -584,7 +584,7 @@ gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* la
                  "model_set lambda");
         CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
     }
-    return GCP_OK;
+    return server_reset(c);   // FedAdam: the server copy starts from the model as set
 }
 
 static gcp_status read_rows(gcp_ctx* c, const void* base, int k, double* out, const char* what) {

@@ -1,0 +1,91 @@
+"""Per-rank worker for the multi-GPU parity test (launched by tests/test_gpu_dist.py
+with torchrun, one process per GPU).  Each rank drives libgcp.so through the C
+ABI on its own GPU (NCCL between ranks) and checks its block against an fp64
+oracle simulation of all P ranks run locally (oracle.MultiRank)."""
+import math
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import gcp_synth  # noqa: E402
+import oracle  # noqa: E402
+
+
+def main():
+    mode = sys.argv[1]
+    rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    import paper_2605_20353_b200 as g
+
+    uid = [g.gcp_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    dims, R, loss = (36, 30, 24), 4, "poisson"
+    subs, vals = gcp_synth.chi_kolda(dims, 3000, R, 1234, loss=loss)
+    subs, vals = subs.numpy(), vals.numpy()
+    blocks, grid = oracle.split_blocks(dims, subs, vals, ws)
+    ggrid, lo, hi = g.gcp_grid_plan(ws, dims)
+    assert tuple(ggrid) == tuple(grid)
+    mine = blocks[rank]
+    assert list(lo[rank]) == mine.lo and list(hi[rank]) == mine.hi
+    bs, bv = mine.sorted()
+
+    ctx = g.Context(local, None, "fp64")
+    ctx.dist_init(ws, rank, uid[0], None, mode)
+    ctx.tensor_create(dims, bs, bv)
+    info = ctx.tensor_info()
+    assert info["nnz"] == mine.nnz and info["nnz_global"] == len(vals)
+    ctx.model_init(R, 77)
+    A0 = oracle.factor_init(77, dims, R)
+    for k in range(3):
+        assert np.array_equal(ctx.model_get(k), A0[k][mine.lo[k]:mine.hi[k]]), "init"
+
+    tau = 2
+    run = oracle.MultiRank(blocks, grid, A0, loss, mode=mode, tau=tau, meta_rate=5e-3)
+    p = q = 600
+    seed, rate = 99, 1e-2
+    ctx.sample("stratified", p, q, seed)
+    if mode != "sync":
+        ctx.dist_set_async(tau, g.adam_params(rate=5e-3))
+    ap = g.adam_params(rate=rate)
+    worst = 0.0
+    for it in range(5):
+        # gradient of this rank's block, before any exchange
+        if mode == "sync":
+            A_rank = run.model_for_rank(rank)
+            pw, qw = oracle.local_counts(mine, p, q, ws, rank)
+            Go, S, _ = oracle.sampled_grad(mine, A_rank, loss, seed, rank, it, pw, qw)
+            ctx.loss_grad(loss)
+            for k in range(3):
+                Gg = ctx.grad_get(k)
+                assert np.all(np.abs(Gg - Go[k]) <= 1e-10 * S[k] + 1e-300), f"grad it={it} k={k}"
+        else:
+            ctx.loss_grad(loss)
+        ctx.adam_step(ap)
+        run.iteration(it, seed, p, q, rate)
+        for k in range(3):
+            want = run.block_rows(rank, k)
+            got = ctx.model_get(k)
+            err = np.abs(got - want).max() / max(1.0, np.abs(want).max())
+            worst = max(worst, err)
+            assert err < 1e-9, f"model it={it} k={k} err={err}"
+    est = ctx.loss_estimate(loss, 1500, 1500, 5)
+    oe, sc = run.estimate(5, 1500, 1500)
+    assert abs(est - oe) <= 1e-10 * sc, (est, oe)
+    ctx.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"DIST-OK mode={mode} P={ws} grid={grid} worst_model_err={worst:.2e}", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
