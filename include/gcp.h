@@ -66,6 +66,11 @@ typedef enum {
 /* Sampling scheme (P:513-537 stratified; P:561-573 semi-stratified). */
 typedef enum { GCP_STRATIFIED = 0, GCP_SEMI_STRATIFIED = 1 } gcp_strategy;
 
+/* Zero-candidate membership structure: a hash set of block keys
+ * (O(1) probe, the default) or the sorted key array searched in O(log N)
+ * (row f4; about 2.6x less memory). */
+typedef enum { GCP_MEMBER_HASH = 0, GCP_MEMBER_SORTED = 1 } gcp_membership;
+
 /* Arithmetic type of factors, gradients, moments (reading R10). */
 typedef enum { GCP_FP32 = 0, GCP_FP64 = 1 } gcp_precision;
 
@@ -152,6 +157,11 @@ gcp_status gcp_dist_set_async(gcp_ctx* ctx, int64_t tau, const gcp_adam_params* 
  * the model.  Blocks; collective for nranks > 1 (global N and M checks). */
 gcp_status gcp_tensor_create(gcp_ctx* ctx, int d, const int64_t* dims, int64_t nnz,
                              const int64_t* subs, const double* vals);
+
+/* Select the zero-test structure the NEXT gcp_tensor_create builds (default
+ * GCP_MEMBER_HASH).  Sampling results are identical for both (membership is a
+ * pure set predicate).  No device work. */
+gcp_status gcp_set_membership(gcp_ctx* ctx, gcp_membership m);
 
 /* Local block summary: nnz_local, block bounds lo/hi (d each, nullable),
  * M_local = prod (hi_k - lo_k) as double, global N.  Blocks. */

@@ -1,6 +1,10 @@
 """Build libgcp.so in-tree: nvcc for sm_100a only, NCCL from the torch wheel.
 
-    python paper_2605_20353_b200/build.py [--force]   (a script: importing the package needs the built library)
+    python paper_2605_20353_b200/build.py [--force] [--variant NAME -DFLAG ...]
+
+(a script: importing the package needs the built library).  A variant build
+(development tuning) compiles with extra -D flags into build_NAME/ and
+libgcp_NAME.so; the binding loads it when GCP_LIB names it.
 """
 from __future__ import annotations
 
@@ -13,8 +17,6 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OUT = PKG / "libgcp.so"
-OBJ = PKG / "build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -37,17 +39,18 @@ def _needs(obj: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, variant: str | None = None, defines=()) -> Path:
     inc, lib = nccl_dirs()
-    OBJ.mkdir(exist_ok=True)
+    objdir = PKG / ("build" if not variant else f"build_{variant}")
+    out = PKG / ("libgcp.so" if not variant else f"libgcp_{variant}.so")
+    objdir.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "gcp.h"]
     srcs = sorted(CSRC.glob("*.cu"))
     jobs = []
     for s in srcs:
-        o = OBJ / (s.stem + ".o")
+        o = objdir / (s.stem + ".o")
         if force or _needs(o, [s] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, f"-I{inc}", "-c", str(s), "-o", str(o)]
-            # the API layer exports the C ABI: default visibility for extern "C" symbols
+            cmd = [NVCC, *ARCH, *FLAGS, *defines, f"-I{inc}", "-c", str(s), "-o", str(o)]
             jobs.append((cmd, o))
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
@@ -59,17 +62,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                     raise RuntimeError(f"nvcc failed for {o.name}:\n{r.stderr}")
                 if verbose and r.stderr.strip():
                     print(r.stderr, file=sys.stderr)
-    objs = [str(OBJ / (s.stem + ".o")) for s in srcs]
-    if force or jobs or not OUT.exists():
-        tmp = OUT.with_suffix(f".{os.getpid()}.tmp")
+    objs = [str(objdir / (s.stem + ".o")) for s in srcs]
+    if force or jobs or not out.exists():
+        tmp = out.with_suffix(f".{os.getpid()}.tmp")
         cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, f"-L{lib}", "-l:libnccl.so.2",
                "-Xlinker", f"-rpath={lib}", "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-        os.replace(tmp, OUT)
-    return OUT
+        os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = sys.argv[1:]
+    variant = None
+    if "--variant" in args:
+        i = args.index("--variant")
+        variant = args[i + 1]
+        args = args[:i] + args[i + 2:]
+    defs = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose=True, variant=variant, defines=defs))

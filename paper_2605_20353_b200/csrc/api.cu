@@ -161,6 +161,8 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     s.kind_nz = kind_nz;
     s.kind_z = kind_z;
     s.stratified = stratified;
+    s.member_sorted = c->member == GCP_MEMBER_SORTED;
+    s.keys = c->d_keys;
     s.err_slot = c->d_err;
     return s;
 }
@@ -316,6 +318,7 @@ void gcp_destroy(gcp_ctx* c) {
     free_model(c);
     cudaFree(c->d_rec);
     cudaFree(c->d_hash);
+    cudaFree(c->d_keys);
     cudaFree(c->d_partials);
     cudaFree(c->d_err);
     if (c->h_scalar) cudaFreeHost(c->h_scalar);
@@ -339,6 +342,13 @@ gcp_status gcp_dist_set_async(gcp_ctx* c, int64_t tau, const gcp_adam_params* se
         c->server = *server;
         c->server_set = true;
     }
+    return GCP_OK;
+}
+
+gcp_status gcp_set_membership(gcp_ctx* c, gcp_membership m) {
+    ENTER(c);
+    if (m != GCP_MEMBER_HASH && m != GCP_MEMBER_SORTED) return set_error(GCP_E_ARG, "gcp_set_membership: bad value");
+    c->member = m;
     return GCP_OK;
 }
 
@@ -507,6 +517,15 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         off += c->rows[k] * c->R_pad;
     }
     c->n_coef = off;
+    {
+        // sync exchange per mode: all-reduce below 16 MB of block rows, else RS/AG
+        const char* env = getenv("GCP_SYNC_EXCHANGE");
+        const std::string pol = env ? env : "auto";
+        for (int k = 0; k < kMaxModes; ++k) {
+            const double mb = k < c->d ? (double)c->rows[k] * c->R_pad * tsz(c) / 1048576.0 : 0;
+            c->ar_mode[k] = pol == "ar" || (pol == "auto" && mb <= 16.0);
+        }
+    }
     const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
     void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C};
     for (void** b : bufs) {
@@ -737,9 +756,14 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     if (sharded) {
         ST_TRY(dist_sync_exchange_pre(c));
         for (int k = 0; k < c->d; ++k) {
-            const int64_t shard = c->rows[k] / c->slice_size[k];
-            seg.start[seg.n] = c->off[k] + (int64_t)c->slice_rank[k] * shard * c->R_pad;
-            seg.len[seg.n] = shard * c->R_pad;
+            if (c->ar_mode[k] || c->slice_size[k] <= 1) {   // replicated rows, all-reduced G
+                seg.start[seg.n] = c->off[k];
+                seg.len[seg.n] = c->rows[k] * c->R_pad;
+            } else {                                         // owned shard of reduce-scattered G
+                const int64_t shard = c->rows[k] / c->slice_size[k];
+                seg.start[seg.n] = c->off[k] + (int64_t)c->slice_rank[k] * shard * c->R_pad;
+                seg.len[seg.n] = shard * c->R_pad;
+            }
             seg.n++;
         }
     } else {

@@ -187,6 +187,10 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
         P.state = 3;
         return P;
     }
+    if (a.member_sorted) {   // row f4: O(log N) search of the sorted keys at resolve time
+        P.state = 4;
+        return P;
+    }
     uint64_t klo, khi;
     const uint64_t b = first_bucket<D>(a, P.c, klo, khi);
     const uint4* h = reinterpret_cast<const uint4*>(a.hash + b);
@@ -194,6 +198,27 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
     P.w1 = __ldg(h + 1);
     P.state = 2;
     return P;
+}
+
+// Row f4: lower-bound binary search of the canonical (sorted) key
+// array; u128 keys are stored as (lo, hi) pairs.
+__device__ __forceinline__ bool sorted_contains(const SampleArgs& a, uint64_t klo, uint64_t khi) {
+    int64_t lo = 0, hi = a.N;   // search [lo, hi)
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        uint64_t mlo, mhi = 0;
+        if (a.key128) {
+            const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(a.keys) + mid);
+            mlo = v.x;
+            mhi = v.y;
+        } else {
+            mlo = __ldg(a.keys + mid);
+        }
+        if (mhi == khi && mlo == klo) return true;
+        if (mhi < khi || (mhi == khi && mlo < klo)) lo = mid + 1;
+        else hi = mid;
+    }
+    return false;
 }
 
 // 0 absent, 1 present, 2 undecided (bucket full of other keys: continue probing)
@@ -212,6 +237,7 @@ __device__ __forceinline__ int bucket_verdict(const SampleArgs& a, const uint4& 
 }
 
 __device__ __forceinline__ bool probe_from(const SampleArgs& a, uint64_t klo, uint64_t khi) {
+    if (a.member_sorted) return sorted_contains(a, klo, khi);
     return a.key128 ? set_contains128(a.hash, a.hash_mask, klo, khi) : set_contains64(a.hash, a.hash_mask, klo);
 }
 
@@ -240,13 +266,18 @@ __device__ __forceinline__ Sample<T, D> resolve_sample(const SampleArgs& a, cons
     o.attempts = 1;
 #pragma unroll
     for (int k = 0; k < D; ++k) o.c[k] = P.c[k];
-    if (P.state != 2) return o;
-    // zero candidate: decide attempt 0 from the prefetched bucket; rejected
-    // candidates redraw all d indices -- rare, handled inline
+    if (P.state != 2 && P.state != 4) return o;
+    // zero candidate: decide attempt 0 from the prefetched bucket (or the sorted
+    // search); rejected candidates redraw all d indices -- rare, inline
     uint64_t klo, khi;
     first_bucket<D>(a, o.c, klo, khi);
-    int v = bucket_verdict(a, P.w0, P.w1, klo, khi);
-    bool present = v == 1 || (v == 2 && probe_from(a, klo, khi));
+    bool present;
+    if (P.state == 4) {
+        present = sorted_contains(a, klo, khi);
+    } else {
+        const int v = bucket_verdict(a, P.w0, P.w1, klo, khi);
+        present = v == 1 || (v == 2 && probe_from(a, klo, khi));
+    }
     for (uint32_t att = 1; present; ++att) {
         if (att >= (uint32_t)kRejectCap) {
             atomicMin(a.err_slot, (unsigned long long)P.slot);

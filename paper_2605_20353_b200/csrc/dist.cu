@@ -57,13 +57,22 @@ gcp_status dist_make_slices(gcp_ctx* c) {
 }
 
 gcp_status dist_sync_exchange_pre(gcp_ctx* c) {
+    // Per mode: small blocks are all-reduced (one latency-bound call, Adam then
+    // runs on the replicated rows); large blocks are reduce-scattered so Adam
+    // and its moments are sharded over the slice group (c->ar_mode, model_init).
     cudaEvent_t ev;
     prof_begin(c, PROF_COMM, &ev);
     NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
     for (int k = 0; k < c->d; ++k) {
         if (c->slice_size[k] <= 1) continue;
-        const size_t shard = (size_t)(c->rows[k] / c->slice_size[k]) * c->R_pad;
         char* base = (char*)c->d_G + (size_t)c->off[k] * tsz(c);
+        if (c->ar_mode[k]) {
+            NCCL_TRY(c, ncclAllReduce(base, base, (size_t)c->rows[k] * c->R_pad, dtype(c), ncclSum, c->slice[k],
+                                      c->stream),
+                     "ncclAllReduce(G)");
+            continue;
+        }
+        const size_t shard = (size_t)(c->rows[k] / c->slice_size[k]) * c->R_pad;
         NCCL_TRY(c, ncclReduceScatter(base, base + (size_t)c->slice_rank[k] * shard * tsz(c), shard, dtype(c), ncclSum,
                                       c->slice[k], c->stream),
                  "ncclReduceScatter(G)");
@@ -74,11 +83,14 @@ gcp_status dist_sync_exchange_pre(gcp_ctx* c) {
 }
 
 gcp_status dist_sync_exchange_post(gcp_ctx* c) {
+    bool any = false;
+    for (int k = 0; k < c->d; ++k) any |= c->slice_size[k] > 1 && !c->ar_mode[k];
+    if (!any) return GCP_OK;
     cudaEvent_t ev;
     prof_begin(c, PROF_COMM, &ev);
     NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
     for (int k = 0; k < c->d; ++k) {
-        if (c->slice_size[k] <= 1) continue;
+        if (c->slice_size[k] <= 1 || c->ar_mode[k]) continue;
         const size_t shard = (size_t)(c->rows[k] / c->slice_size[k]) * c->R_pad;
         char* base = (char*)c->d_A + (size_t)c->off[k] * tsz(c);
         NCCL_TRY(c, ncclAllGather(base + (size_t)c->slice_rank[k] * shard * tsz(c), base, shard, dtype(c), c->slice[k],

@@ -16,8 +16,18 @@ namespace gcp {
 constexpr int kMaxModes = 8;          // array capacity
 constexpr int kMaxD = 6;              // d <= 6 on the device path (record = value + d coords <= 32 B)
 constexpr int kRejectCap = 1000;      // reading R5
-constexpr int kBlock = 256;           // threads per CTA of the sample kernels
-constexpr int kSampleMinBlocks = 2;   // >= 16 resident warps per SM (register cap 128)
+#ifndef GCP_BLOCK
+#define GCP_BLOCK 256
+#endif
+#ifndef GCP_MINB
+#define GCP_MINB 2
+#endif
+#ifndef GCP_RBREG
+#define GCP_RBREG 8
+#endif
+constexpr int kBlock = GCP_BLOCK;          // threads per CTA of the sample kernels
+constexpr int kSampleMinBlocks = GCP_MINB; // resident CTAs per SM the register budget must allow
+constexpr int kRowRegBudget = GCP_RBREG;   // 16-B row vectors per lane kept in flight per batch
 constexpr double kHashLoad = 0.5;     // target hash-set load factor
 
 enum Kind : uint32_t { KIND_GRAD_NZ = 0, KIND_GRAD_Z = 1, KIND_F_NZ = 2, KIND_F_Z = 3, KIND_INIT = 4 };
@@ -37,6 +47,8 @@ struct SampleArgs {
     uint64_t seed;
     uint32_t rank, it, kind_nz, kind_z;
     int stratified;           // 0: semi-stratified (no membership test)
+    int member_sorted;        // 1: binary search of `keys` instead of the hash set (row f4)
+    const uint64_t* keys;     // sorted block keys (u64, or (lo,hi) pairs for u128)
     unsigned long long* err_slot;  // min zero slot that hit the rejection cap (ULLONG_MAX = none)
 };
 
@@ -73,6 +85,7 @@ struct gcp_ctx {
     ncclComm_t world = nullptr;
     ncclComm_t slice[gcp::kMaxModes] = {nullptr};
     int slice_size[gcp::kMaxModes] = {0}, slice_rank[gcp::kMaxModes] = {0};
+    bool ar_mode[gcp::kMaxModes] = {false};   // sync exchange of mode k: all-reduce (else RS/AG)
     int64_t tau = 0;
     gcp_adam_params server{};
     bool server_set = false;
@@ -88,6 +101,8 @@ struct gcp_ctx {
     uint64_t* d_hash = nullptr;
     uint64_t hash_slots = 0;
     int key128 = 0;
+    gcp_membership member = GCP_MEMBER_HASH;   // zero-test structure built at ingest
+    uint64_t* d_keys = nullptr;                // sorted keys (GCP_MEMBER_SORTED)
     // ---- model
     bool have_model = false;
     int R = 0, R_pad = 0;

@@ -102,13 +102,25 @@ __global__ void k_hash_insert(int64_t n, const uint64_t* __restrict__ klo, const
     }
 }
 
-__global__ void k_contains(const KeyArgs ka, int64_t n, const int64_t* __restrict__ coords, const uint64_t* h,
-                           uint64_t mask, int key128, int8_t* out) {
+// sorted key array for the binary-search zero test (row f4): u64, or (lo, hi) pairs
+__global__ void k_store_keys(int64_t n, const uint64_t* __restrict__ klo, const uint64_t* __restrict__ khi,
+                             uint64_t* __restrict__ out) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        if (khi) {
+            out[2 * x] = klo[x];
+            out[2 * x + 1] = khi[x];
+        } else {
+            out[x] = klo[x];
+        }
+    }
+}
+
+__global__ void k_contains(const KeyArgs ka, int64_t n, const int64_t* __restrict__ coords, const SampleArgs sa,
+                           int8_t* out) {
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
         unsigned __int128 key = 0;
         for (int k = 0; k < ka.d; ++k) key = key * ka.bdim[k] + (uint64_t)(coords[x * ka.d + k] - ka.lo[k]);
-        out[x] = key128 ? set_contains128(h, mask, (uint64_t)key, (uint64_t)(key >> 64))
-                        : set_contains64(h, mask, (uint64_t)key);
+        out[x] = probe_from(sa, (uint64_t)key, (uint64_t)(key >> 64));
     }
 }
 
@@ -133,8 +145,14 @@ static int bits_for(unsigned __int128 v) {   // bits needed to represent v - 1 (
 cudaError_t launch_contains(gcp_ctx* c, int64_t n, const int64_t* coords, int8_t* out) {
     if (n == 0) return cudaSuccess;
     const KeyArgs ka = key_args(c);
-    k_contains<<<(int)std::min<int64_t>((n + 255) / 256, 65535), 256, 0, c->stream>>>(
-        ka, n, coords, c->d_hash, c->hash_slots - 1, c->key128, out);
+    SampleArgs sa{};
+    sa.N = c->N;
+    sa.hash = c->d_hash;
+    sa.hash_mask = c->hash_slots - 1;
+    sa.key128 = c->key128;
+    sa.member_sorted = c->member == GCP_MEMBER_SORTED;
+    sa.keys = c->d_keys;
+    k_contains<<<(int)std::min<int64_t>((n + 255) / 256, 65535), 256, 0, c->stream>>>(ka, n, coords, sa, out);
     return cudaGetLastError();
 }
 
@@ -168,14 +186,18 @@ gcp_status ingest(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs
 
     uint32_t* new_rec = nullptr;
     uint64_t* new_hash = nullptr;
+    uint64_t* new_keys = nullptr;
+    const bool sorted_member = c->member == GCP_MEMBER_SORTED;
     const int val_words = tw / 4;
     const int rec_words = (val_words + d <= 4) ? 4 : 8;
+    if (sorted_member) slots = 4;   // no hash set: a 4-slot empty table keeps the pointer valid
 
     CK(cudaMalloc(&d_flags, sizeof(unsigned)));
     CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
     CK(cudaMalloc(&new_rec, (size_t)std::max<int64_t>(nnz, 1) * rec_words * 4));
     CK(cudaMalloc(&new_hash, (size_t)slots * 8 * (k128 ? 2 : 1)));
     CK(cudaMemsetAsync(new_hash, 0xFF, (size_t)slots * 8 * (k128 ? 2 : 1), st));
+    CK(cudaMalloc(&new_keys, (size_t)(sorted_member ? std::max<int64_t>(nnz, 1) : 1) * 8 * (k128 ? 2 : 1)));
     if (nnz > 0) {
         CK(cudaMalloc(&d_subs, (size_t)nnz * d * sizeof(int64_t)));
         CK(cudaMalloc(&d_vals, (size_t)nnz * sizeof(double)));
@@ -245,7 +267,10 @@ gcp_status ingest(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs
                                                       d_vals, new_rec);
             CK(cudaGetLastError());
             c->launches++;
-            k_hash_insert<<<nb, 256, 0, st>>>(nnz, sorted_lo, sorted_hi, new_hash, slots - 1);
+            if (sorted_member)
+                k_store_keys<<<nb, 256, 0, st>>>(nnz, sorted_lo, sorted_hi, new_keys);
+            else
+                k_hash_insert<<<nb, 256, 0, st>>>(nnz, sorted_lo, sorted_hi, new_hash, slots - 1);
             CK(cudaGetLastError());
             c->launches++;
             CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
@@ -261,6 +286,7 @@ cleanup:
     if (err != cudaSuccess || status != GCP_OK) {
         cudaFree(new_rec);
         cudaFree(new_hash);
+        cudaFree(new_keys);
         if (err == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             return set_error(GCP_E_OOM, "gcp_tensor_create: out of device memory");
@@ -271,8 +297,10 @@ cleanup:
     // commit
     cudaFree(c->d_rec);
     cudaFree(c->d_hash);
+    cudaFree(c->d_keys);
     c->d_rec = new_rec;
     c->d_hash = new_hash;
+    c->d_keys = new_keys;
     c->key128 = k128 ? 1 : 0;
     c->val_words = val_words;
     c->rec_words = rec_words;

@@ -59,14 +59,24 @@ __device__ __forceinline__ void ldg_vec<double, 2>(double (&dst)[2], const doubl
 // processes the 32 samples in GL rounds of 32/GL samples, a sample per group of
 // GL lanes, each lane owning NV 16-byte vectors of every factor row.  Rounds are
 // handled RB at a time with all their row loads issued before any arithmetic.
+// Register budget per instantiation: small row footprints (D*NV <= 3) run at
+// 4 CTAs/SM (64 regs) with one row batch in flight; larger ones at
+// kSampleMinBlocks with kRowRegBudget row vectors in flight (B200 K2 tuning,
+// profiles/r01_summary.md).
+template <int D, int NV> struct SampleGeom {
+    static constexpr bool small = D * NV <= 3;
+    static constexpr int minb = small ? 4 : kSampleMinBlocks;
+    static constexpr int rowregs = small ? 4 : kRowRegBudget;
+};
+
 template <typename T, int D, int GL, int NV>
-__global__ void __launch_bounds__(kBlock, kSampleMinBlocks) k_sample(const SampleArgs sa, const ModelArgs ma,
+__global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
                                                    const KParams<T> kp) {
     constexpr int VE = Vec16<T>::n;
     constexpr int SPR = 32 / GL;                 // samples per round
-    // rounds per load batch: bounded so the row registers (RB*D*NV*16 B) stay < ~64 regs
-    // (a power of two, so it divides GL)
-    constexpr int RB_REG = 8 / (D * NV);
+    // rounds per load batch: bounded so the row registers (RB*D*NV*16 B) fit the
+    // budget (a power of two, so it divides GL)
+    constexpr int RB_REG = SampleGeom<D, NV>::rowregs / (D * NV);
     constexpr int RB_CAP = GL < 4 ? GL : 4;
     constexpr int RB = RB_REG >= 4 && RB_CAP >= 4 ? 4 : (RB_REG >= 2 && RB_CAP >= 2 ? 2 : 1);
     const int lane = threadIdx.x & 31;

@@ -9,11 +9,12 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "libgcp.so"
+_LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GCP_LIB", "libgcp.so")
 
 GCP_OK = 0
 STATUS = {0: "GCP_OK", 1: "GCP_E_ARG", 2: "GCP_E_RANGE", 3: "GCP_E_DUP", 4: "GCP_E_NO_NONZEROS",
@@ -31,7 +32,8 @@ SYMBOLS = ["gcp_create", "gcp_destroy", "gcp_last_error", "gcp_grid_plan", "gcp_
            "gcp_tensor_export_sorted", "gcp_tensor_contains", "gcp_model_init", "gcp_model_set",
            "gcp_model_get", "gcp_sample", "gcp_sample_export", "gcp_loss_grad", "gcp_grad_get",
            "gcp_adam_step", "gcp_loss_estimate", "gcp_fit_begin", "gcp_fit_epoch", "gcp_fit",
-           "gcp_counters", "gcp_profile_enable", "gcp_profile_get"]
+           "gcp_counters", "gcp_profile_enable", "gcp_profile_get", "gcp_set_membership"]
+MEMBERSHIP = {"hash": 0, "sorted": 1}
 
 
 class GcpError(RuntimeError):
@@ -88,6 +90,7 @@ def load():
         "gcp_counters": [vp, C.POINTER(C.c_uint32), i64p, i64p],
         "gcp_profile_enable": [vp, C.c_int],
         "gcp_profile_get": [vp, C.c_int, dp, i64p, C.c_int],
+        "gcp_set_membership": [vp, C.c_int],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -177,6 +180,9 @@ class Context:
              "gcp_dist_set_async")
 
     # ---- tensor
+    def set_membership(self, m):
+        _chk(lib.gcp_set_membership(self.h, MEMBERSHIP[m]), "gcp_set_membership")
+
     def tensor_create(self, dims, subs, vals):
         dims_a = _i64(dims)
         subs_a = _i64(subs).reshape(-1)

@@ -224,6 +224,41 @@ def test_u128_keys_lbnl_shape(gcp, orc):
     _grad_check(G, Go, S, 1e-4, "u128 bernoulli")
 
 
+@pytest.mark.parametrize("shape", ["c1", "lbnl"])
+def test_sorted_membership_same_draws(gcp, orc, shape):
+    """Row f4: the binary-search zero test gives the same samples as the hash set."""
+    if shape == "c1":
+        dims = (20, 30, 40)
+        subs, vals = _tensor("poisson")
+        R = 4
+    else:
+        dims = gcp_synth.CONFIGS["c3"]["dims"]
+        rng = np.random.default_rng(6)
+        subs = np.unique(np.stack([rng.integers(0, I, 20000) for I in dims], 1), axis=0)
+        vals = np.ones(len(subs))
+        R = 10
+    t = orc.Tensor(dims, subs, vals)
+    c = gcp.Context(0, None, "fp32")
+    c.set_membership("sorted")
+    c.tensor_create(dims, subs, vals)
+    c.model_init(R, 2001)
+    assert c.tensor_contains(subs).all()
+    rng = np.random.default_rng(1)
+    cand = np.stack([rng.integers(0, I, 4000) for I in dims], 1)
+    cand[:1000] = subs[:1000]
+    assert np.array_equal(c.tensor_contains(cand), np.array([t.contains(x) for x in cand]))
+    c.sample("stratified", 2000, 2000, 3001)
+    gs, gj, _, ga = c.sample_export(1, 0, 2000)
+    os_, oj, _, oa = orc.sample_export(t, 1, 3001, 0, 0, 2000, 0, 2000)
+    assert np.array_equal(gs, os_) and np.array_equal(ga, oa)
+    A = _model(c, len(dims))
+    loss = "poisson" if shape == "c1" else "bernoulli"
+    c.loss_grad(loss)
+    G = [c.grad_get(k) for k in range(len(dims))]
+    Go, S, _ = orc.sampled_grad(t, A, loss, 3001, 0, 0, 2000, 2000)
+    _grad_check(G, Go, S, 1e-4, "sorted membership")
+
+
 def test_fit_runs_and_decreases(gcp, orc):
     dims = (20, 30, 40)
     subs, vals = _tensor("poisson")
