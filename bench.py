@@ -34,6 +34,14 @@ import torch  # noqa: E402
 
 import gcp_synth  # noqa: E402
 
+_T0 = time.time()
+
+
+def log(*a):
+    """Progress to stderr (stdout carries only the JSON line)."""
+    print(f"[bench {time.time() - _T0:7.1f}s]", *a, file=sys.stderr, flush=True)
+
+
 METRIC = "GCP-Adam epochs/sec and sampled-gradient samples/sec (1/2/4/8 B200); HBM GB/s"
 ITERS = 100  # iterations per epoch (P:868-869)
 
@@ -173,26 +181,31 @@ def block_of(subs, vals, lo, hi):
 
 
 # ------------------------------------------------------------------ reference arm (CPU oracle)
-def run_oracle_sample(name, subs_h, vals_h, steps, warmup, sample_n):
+def run_oracle_sample(name, subs_h, vals_h, steps, warmup, sample_n, lo=None, hi=None):
     """Time the fp64 oracle, as it stands, on a bounded sample of one epoch of
     workload `name`: per step one sampled gradient with p'=q'=sample_n, one Adam
     pass over all coefficients, one loss estimate with f'=sample_n; extrapolated
-    to the epoch (100 iterations at p=q, f-samples f)."""
+    to the epoch (100 iterations at p=q, f-samples f).  lo/hi: a block of the
+    tensor (its nonzeros in subs_h) instead of the whole."""
     import oracle
     w = workload(name)
     t0 = time.time()
-    t = oracle.Tensor(w["dims"], subs_h, vals_h)
+    t = oracle.Tensor(w["dims"], subs_h, vals_h, lo, hi)
     setup = time.time() - t0
     A = oracle.factor_init(gcp_synth.SEEDS[name]["model"], w["dims"], w["R"])
-    flat = np.concatenate([a.ravel() for a in A])
+    flat = np.concatenate([a.ravel() for a in A])   # the whole model: Adam runs over all of it
     B, Cm = np.zeros_like(flat), np.zeros_like(flat)
+    Gf = np.zeros_like(flat)
+    offs = np.cumsum([0] + [int(I) * w["R"] for I in w["dims"]])
+    blo = [0] * w["d"] if lo is None else lo
     times = []
     for s in range(warmup + steps):
         t1 = time.perf_counter()
         G, _, _ = oracle.sampled_grad(t, A, w["loss"], gcp_synth.SEEDS[name]["sample"], 0, s, sample_n, sample_n,
                                       with_scale=False)
         tg = time.perf_counter() - t1
-        Gf = np.concatenate([g.ravel() for g in G])
+        for k in range(w["d"]):   # the block's rows into the global gradient
+            Gf[offs[k] + blo[k] * w["R"]: offs[k] + blo[k] * w["R"] + G[k].size] = G[k].ravel()
         t2 = time.perf_counter()
         oracle.adam(flat, Gf, B, Cm, s + 1, 1e-3, 0.9, 0.999, 1e-8, oracle.loss_lower(w["loss"]))
         ta = time.perf_counter() - t2
@@ -215,9 +228,10 @@ def reference_arm(args, ws, rank):
     subs_h, vals_h = subs.cpu().numpy(), vals.cpu().numpy()
     del subs, vals
     n = args.cpu_sample
-    r = run_oracle_sample(name, subs_h, vals_h, args.steps, args.warmup, n)
+    subs_h, vals_h, lo, hi, what = oracle_sample_block(w, subs_h, vals_h)
+    r = run_oracle_sample(name, subs_h, vals_h, args.steps, args.warmup, n, lo, hi)
     eps = 1.0 / r["epoch_s"]
-    sample = (f"oracle (fp64, 1 thread) per step: 1 sampled gradient with p'=q'={n}, 1 Adam pass over all "
+    sample = (f"oracle (fp64, 1 thread) on {what}, per step: 1 sampled gradient with p'=q'={n}, 1 Adam pass over all "
               f"{sum(w['dims']) * w['R']} coefficients, 1 loss estimate with f'={n}; extrapolated to one epoch "
               f"(100 iterations at p=q={w['s']:.0e}, f={w['f']:.0e})")
     line = {"impl": "reference", "metric": METRIC, "value": eps, "unit": "epochs/s", "n_gpus": args.gpus,
@@ -264,15 +278,22 @@ def main():
     ctx.dist_init(ws, rank, uid, None, args.mode)
     grid, lo, hi = g.gcp_grid_plan(ws, w["dims"])
 
+    log("generate", name)
     subs, vals, gen_s = make_tensor(name, f"cuda:{dev}")
-    bs, bv = block_of(subs, vals, lo[rank], hi[rank])
-    del subs, vals
-    subs_h = bs.cpu().pin_memory()
-    vals_h = bv.cpu().pin_memory()
+    log("generated", len(vals))
+    if ws > 1:
+        subs, vals = block_of(subs, vals, lo[rank], hi[rank])
+    subs_h = torch.empty(subs.shape, dtype=subs.dtype, pin_memory=True)
+    subs_h.copy_(subs)
+    del subs
+    vals_h = torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True)
+    vals_h.copy_(vals)
+    del vals
+    log("host copy (pinned)")
     nnz_local = len(vals_h)
-    del bs, bv
     torch.cuda.empty_cache()
     t0 = time.time()
+    log("ingest", nnz_local)
     ctx.tensor_create_ptr(w["dims"], nnz_local, subs_h.data_ptr(), vals_h.data_ptr())
     ingest_s = time.time() - t0
     ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
@@ -280,6 +301,7 @@ def main():
                         f_nz=w["f"], f_z=w["f"], loss=w["loss"], seed=gcp_synth.SEEDS[name]["sample"], fseed=2,
                         rate=1e-3, tau=args.tau if args.mode != "sync" else 0, meta_rate=1e-3)
     ctx.fit_begin(fp)
+    log("warm-up")
     for _ in range(args.warmup):
         ctx.fit_epoch()
     ctx.profile_enable(True)
@@ -318,17 +340,18 @@ def main():
     if tr.exists():
         traffic = json.loads(tr.read_text()).get("k2_dram_bytes_per_launch")
     # ---- e2e: the public API from pinned host buffers, copies inside the timed region
+    A0 = [ctx.model_get(k) for k in range(w["d"])] if not args.no_e2e else None
+    ctx.close()
+    torch.cuda.empty_cache()
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, ctx, w, name, fp, subs_h, vals_h, dev, stream, ws, args)
+        log("e2e")
+        e2e = run_e2e(g, A0, w, fp, subs_h, vals_h, dev, stream, ws, rank, args)
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        r = run_oracle_sample(name, subs_h.numpy(), vals_h.numpy(), 2, 1, args.cpu_sample)
-        cpu = {"value": 1.0 / r["epoch_s"], "unit": "epochs/s", "cores": 1, "kind": "oracle",
-               "sample": (f"1 sampled gradient (p'=q'={args.cpu_sample}) + 1 Adam pass + 1 loss estimate "
-                          f"(f'={args.cpu_sample}) per step, median of 2 steps after 1 warm-up, extrapolated to "
-                          f"one epoch of 100 iterations at p=q={w['s']:.0e}; fp64 single-thread C oracle")}
+        log("cpu baseline")
+        cpu = cpu_baseline(g, name, w, subs_h, vals_h, args)
     if rank == 0:
         clocks = clk.summary()
         line = {
@@ -339,7 +362,9 @@ def main():
                        "R": w["R"], "loss": w["loss"], "p": w["s"], "q": w["s"], "f_nz": w["f"], "f_z": w["f"],
                        "iters_per_epoch": ITERS, "grid": list(grid), "dist_mode": args.mode,
                        "parallelism": f"grid{'x'.join(map(str, grid))}-{args.mode}" if ws > 1 else "single-gpu",
-                       "l2": "inputs larger than L2 (COO records + hash set >> 126 MB); factors stay L2-resident",
+                       "l2": ("inputs larger than L2 (COO records + hash set >> 126 MB); factors "
+                              + ("stay L2-resident" if sum(w["dims"]) * w["R"] * 4 < 32e6
+                                 else "and gradient far exceed L2")),
                        "nnz_local_rank0": nnz_local},
             "samples_per_s": samples_per_s,
             "hbm_gbs_k2_algorithmic": achieved,
@@ -355,32 +380,62 @@ def main():
             "setup_s": {"generate": gen_s, "ingest": ingest_s},
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 
 
-def run_e2e(g, ctx, w, name, fp, subs_h, vals_h, dev, stream, ws, args):
-    """Per step: ingest the COO from pinned host memory (H2D), upload the initial
-    factors from host (H2D), fit_begin + one epoch, read back the factors and the
-    loss (D2H) -- the job a user runs through the public API."""
-    A0 = [ctx.model_get(k) for k in range(w["d"])]
+def oracle_sample_block(w, subs, vals):
+    """Whole tensor, or beyond 2e8 nonzeros the rank-0 block of the oracle's own
+    64-way grid plan (same density; the oracle's sort stays small)."""
+    if w["nnz"] <= 200_000_000:
+        return subs, vals, None, None, "the full tensor"
+    import oracle
+    grid, _ = oracle.grid_plan(64, w["dims"])
+    lo, hi = oracle.block_bounds(w["dims"], grid, 0)
+    m = np.ones(len(vals), bool)
+    for k in range(w["d"]):
+        m &= (subs[:, k] >= lo[k]) & (subs[:, k] < hi[k])
+    return subs[m], vals[m], lo, hi, f"the rank-0 block of a 64-way grid ({int(m.sum())} nnz, {lo}-{hi})"
+
+
+def cpu_baseline(g, name, w, subs_h, vals_h, args):
+    """The oracle, as it stands, on a bounded sample of this workload.  Tensors
+    beyond 2e8 nonzeros are sampled as the rank-0 block of a 64-way grid (same
+    density, per-rank sample arithmetic) so the oracle's own sort stays small."""
+    subs, vals, lo, hi, what = oracle_sample_block(w, subs_h.numpy(), vals_h.numpy())
+    r = run_oracle_sample(name, subs, vals, 2, 1, args.cpu_sample, lo, hi)
+    return {"value": 1.0 / r["epoch_s"], "unit": "epochs/s", "cores": 1, "kind": "oracle",
+            "sample": (f"on {what}: 1 sampled gradient (p'=q'={args.cpu_sample}) + 1 Adam pass + 1 loss estimate "
+                       f"(f'={args.cpu_sample}) per step, median of 2 steps after 1 warm-up, extrapolated to one "
+                       f"epoch of 100 iterations at p=q={w['s']:.0e}; fp64 single-thread C oracle"),
+            "oracle_setup_s": r["setup_s"]}
+
+
+def run_e2e(g, A0, w, fp, subs_h, vals_h, dev, stream, ws, rank, args):
+    """Per step, the job a user runs through the public API: create a context,
+    ingest the COO from pinned host memory (H2D), upload the initial factors
+    (H2D), fit_begin + one epoch, read back the factors and the loss (D2H),
+    destroy the context.  Wall time of the whole job, max over ranks."""
     h2d = subs_h.numel() * 8 + vals_h.numel() * 8 + sum(a.size * 8 for a in A0)
     d2h = sum(a.size * 8 for a in A0) + 8
     steps = max(1, min(args.steps, 3))
     times = []
     for s in range(steps + 1):
+        uid = bcast_bytes(ws, rank, g.gcp_nccl_unique_id() if (rank == 0 and ws > 1) else None)
         barrier(ws)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        ctx = g.Context(dev, stream.cuda_stream, args.precision)
+        ctx.dist_init(ws, rank, uid, None, args.mode)
         ctx.tensor_create_ptr(w["dims"], vals_h.numel(), subs_h.data_ptr(), vals_h.data_ptr())
-        ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
+        ctx.model_init(w["R"], 0)
         for k in range(w["d"]):
             ctx.model_set(k, A0[k])
         ctx.fit_begin(fp)
-        est, _, _ = ctx.fit_epoch()
+        ctx.fit_epoch()
         _ = [ctx.model_get(k) for k in range(w["d"])]
+        ctx.close()
         torch.cuda.synchronize()
         dt = allmax(ws, time.perf_counter() - t0)
         if s > 0:
@@ -388,7 +443,8 @@ def run_e2e(g, ctx, w, name, fp, subs_h, vals_h, dev, stream, ws, args):
     t = float(np.median(times))
     return {"value": 1.0 / t, "unit": "epochs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": t * 1e3, "steps": steps,
-            "includes": "H2D COO + ingest (sort, dup check, hash) + H2D factors + F0 estimate + 1 epoch + D2H"}
+            "includes": "context + H2D COO + ingest (sort, dup check, hash) + H2D factors + F0 estimate + "
+                        "1 epoch + D2H factors/loss"}
 
 
 if __name__ == "__main__":

@@ -63,13 +63,30 @@ def _unlin(keys, dims):
     return out
 
 
+def _merge2(hi, lo, cnt):
+    """Merge duplicate (hi, lo) keys, summing counts; result sorted by (hi, lo)."""
+    o = torch.argsort(lo, stable=True)
+    hi, lo, cnt = hi[o], lo[o], cnt[o]
+    o = torch.argsort(hi, stable=True)
+    hi, lo, cnt = hi[o], lo[o], cnt[o]
+    del o
+    new = torch.ones(hi.numel(), dtype=torch.bool, device=hi.device)
+    new[1:] = (hi[1:] != hi[:-1]) | (lo[1:] != lo[:-1])
+    seg = torch.cumsum(new, 0) - 1
+    cu = torch.zeros(int(seg[-1]) + 1 if seg.numel() else 0, dtype=torch.int64, device=hi.device)
+    cu.index_add_(0, seg, cnt)
+    return hi[new], lo[new], cu
+
+
 def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, boost=10.0,
-              tol=0.005, max_rounds=64):
+              tol=0.005, max_rounds=64, force_wide=False):
     """Return (subs int64 [N, d], vals float64 [N]) as torch tensors on `device`.
 
-    Requires prod(dims) < 2^63 (the merge key is int64)."""
+    Duplicate draws merge on an int64 mixed-radix key when prod(dims) < 2^62,
+    else on the pair (i_1, key of the other modes) (needs prod(dims[1:]) < 2^63)."""
     dims = [int(i) for i in dims]
-    assert math.prod(dims) < 2 ** 63, "merge key would overflow int64"
+    wide = force_wide or math.prod(dims) >= 2 ** 62
+    assert not wide or math.prod(dims[1:]) < 2 ** 63
     assert nnz <= math.prod(dims)
     g = _gen(seed, device)
     cdfs = []
@@ -83,44 +100,105 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
         c = torch.cumsum(A, dim=1)
         c[:, -1] = 1.0
         cdfs.append((c + torch.arange(R, device=device, dtype=torch.float64)[:, None]).reshape(-1))
-    keys = torch.empty(0, dtype=torch.int64, device=device)
-    counts = torch.empty(0, dtype=torch.int64, device=device)
+        del A, c
     lo_target = int(math.floor(nnz * (1 - tol)))
-    want = nnz
-    for _ in range(max_rounds):
-        n_draw = max(1024, int((want - keys.numel()) * 1.02) + 64)
-        r = torch.randint(0, R, (n_draw,), generator=g, device=device)
-        cols = []
-        for k, I in enumerate(dims):
-            u = torch.rand(n_draw, generator=g, device=device, dtype=torch.float64) + r.double()
-            i = torch.searchsorted(cdfs[k], u, right=True) - r * I
-            cols.append(i.clamp_(0, I - 1))
-        del r
-        nk = _lin_keys(torch.stack(cols, 1), dims)
-        del cols
-        allk = torch.cat([keys, nk])
-        allc = torch.cat([counts, torch.ones_like(nk)])
-        keys, inv = torch.unique(allk, sorted=True, return_inverse=True)
-        counts = torch.zeros_like(keys).index_add_(0, inv, allc)
-        del allk, allc, inv, nk
-        if keys.numel() >= lo_target:
-            break
-        # far below target (dense, collision-heavy tensor): draw more next round
+    if not wide:
+        keys = torch.empty(0, dtype=torch.int64, device=device)
+        counts = torch.empty(0, dtype=torch.int64, device=device)
         want = nnz
-    if keys.numel() > nnz * (1 + tol):
-        # deterministic thinning to the tolerance band (keeps sorted order)
-        perm = torch.randperm(keys.numel(), generator=g, device=device)[:nnz]
-        perm, _ = torch.sort(perm)
+        for _ in range(max_rounds):
+            n_draw = max(1024, int((want - keys.numel()) * 1.02) + 64)
+            cols = _draw(cdfs, dims, R, n_draw, g, device)
+            nk = _lin_keys(torch.stack(cols, 1), dims)
+            del cols
+            allk = torch.cat([keys, nk])
+            allc = torch.cat([counts, torch.ones_like(nk)])
+            del nk
+            keys, inv = torch.unique(allk, sorted=True, return_inverse=True)
+            counts = torch.zeros_like(keys).index_add_(0, inv, allc)
+            del allk, allc, inv
+            if keys.numel() >= lo_target:
+                break
+        if keys.numel() > nnz * (1 + tol):
+            # deterministic thinning to the tolerance band (keeps sorted order)
+            perm = torch.randperm(keys.numel(), generator=g, device=device)[:nnz]
+            perm, _ = torch.sort(perm)
+            keys, counts = keys[perm], counts[perm]
+        # shuffle so that ingest sees an unsorted list, like a file would be
+        perm = torch.randperm(keys.numel(), generator=g, device=device)
         keys, counts = keys[perm], counts[perm]
-    # shuffle so that ingest sees an unsorted list, like a file would be
-    perm = torch.randperm(keys.numel(), generator=g, device=device)
-    keys, counts = keys[perm], counts[perm]
-    subs = _unlin(keys, dims)
+        del perm
+        subs = _unlin(keys, dims)
+        del keys
+    else:
+        # Billion-scale path: draws arrive in rounds of <= 4e8 and are split into
+        # i_1-range partitions (duplicates share i_1) of < 2^31 entries each, so
+        # every sort stays below 2^31 elements.
+        nparts = max(1, -(-nnz // 200_000_000))
+        edges = [dims[0] * j // nparts for j in range(nparts + 1)]
+        parts = [(torch.empty(0, dtype=torch.int64, device=device),) * 3 for _ in range(nparts)]
+        total = 0
+        for _ in range(max_rounds):
+            left = max(1024, int((nnz - total) * 1.02) + 64)
+            while left > 0:
+                n_draw = min(left, 400_000_000)
+                left -= n_draw
+                cols = _draw(cdfs, dims, R, n_draw, g, device)
+                nlo = cols[1].clone()
+                for k in range(2, len(dims)):
+                    nlo = nlo * dims[k] + cols[k]
+                nhi = cols[0]
+                del cols
+                pid = torch.bucketize(nhi, torch.tensor(edges[1:-1], device=device), right=True)
+                for j in range(nparts):
+                    m = pid == j
+                    ph, pl, pc = parts[j]
+                    parts[j] = _merge2(torch.cat([ph, nhi[m]]), torch.cat([pl, nlo[m]]),
+                                       torch.cat([pc, torch.ones(int(m.sum()), dtype=torch.int64, device=device)]))
+                del nhi, nlo, pid
+            total = sum(p[0].numel() for p in parts)
+            if total >= lo_target:
+                break
+        keep = nnz / total if total > nnz * (1 + tol) else None
+        subs_l, cnt_l = [], []
+        for j in range(nparts):
+            ph, pl, pc = parts[j]
+            parts[j] = None
+            if keep is not None:   # Bernoulli thinning to the tolerance band
+                m = torch.rand(ph.numel(), generator=g, device=device) < keep
+                ph, pl, pc = ph[m], pl[m], pc[m]
+            perm = torch.randperm(ph.numel(), generator=g, device=device)   # shuffle within the partition
+            ph, pl, pc = ph[perm], pl[perm], pc[perm]
+            sj = torch.empty((ph.numel(), len(dims)), dtype=torch.int64, device=device)
+            sj[:, 0] = ph
+            sj[:, 1:] = _unlin(pl, dims[1:])
+            subs_l.append(sj)
+            cnt_l.append(pc)
+            del ph, pl, perm
+        subs = torch.cat(subs_l)
+        del subs_l
+        counts = torch.cat(cnt_l)
+        del cnt_l
     if loss == "bernoulli":
-        vals = torch.ones(keys.numel(), dtype=torch.float64, device=device)
+        vals = torch.ones(counts.numel(), dtype=torch.float64, device=device)
     else:
         vals = counts.double()
     return subs, vals
+
+
+def _draw(cdfs, dims, R, n, g, device):
+    """n Chi-Kolda draws: r ~ uniform(R) (lambda_r = 1/R), then i_k ~ A^(k)(:, r)
+    by inverse CDF."""
+    r = torch.randint(0, R, (n,), generator=g, device=device)
+    cols = []
+    for k, I in enumerate(dims):
+        u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+        u += r
+        i = torch.searchsorted(cdfs[k], u, right=True)
+        del u
+        i -= r * I
+        cols.append(i.clamp_(0, I - 1))
+    return cols
 
 
 def uniform_sparse(dims, nnz, seed, values="normal"):

@@ -341,7 +341,7 @@ def full_grad(t, A, loss, lam=None):
 def adam(A, G, B, Cm, t, alpha, beta1=0.9, beta2=0.999, eps=1e-8, lower=-math.inf):
     """Alg. 1 in place on flat fp64 arrays; t = step number after increment."""
     for a in (A, G, B, Cm):
-        assert a.dtype == np.float64 and a.flags.c_contiguous
+        assert a.dtype == np.float64 and a.flags.c_contiguous and a.size == A.size
     lib().orc_adam(A.size, _p(A, C.c_double), _p(G, C.c_double), _p(B, C.c_double),
                    _p(Cm, C.c_double), t, alpha, beta1, beta2, eps, lower)
 

@@ -1,8 +1,15 @@
 // ingest.cu -- row a0 (untimed setup): host COO -> device, validation, canonical
 // lexicographic order (reading R15), duplicate check, AoS
-// records, and the open-addressing hash set of block keys.
+// records, and the zero-test structure: an open-addressing hash set of block
+// keys or the sorted key array (row f4).
+//
+// Memory-lean for billion-nonzero tensors: the host int64 coordinates stream
+// through a fixed staging buffer and are converted on the fly to 32-bit local
+// coordinates; the sort carries a 32-bit permutation when N < 2^32; the
+// records and the hash set are built after the sort scratch is released.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -19,37 +26,58 @@ struct KeyArgs {
 
 enum : unsigned { BAD_RANGE = 1u, BAD_VALUE = 2u, BAD_DUP = 4u };
 
-// Validate every coordinate / value and form the mixed-radix block key
-// ((c_1 b_2 + c_2) b_3 + ...) b_d + c_d of the local coordinates c = i - lo.
-__global__ void k_keys(const KeyArgs ka, int64_t n, const int64_t* __restrict__ subs,
-                       const double* __restrict__ vals, uint64_t* __restrict__ klo, uint64_t* __restrict__ khi,
-                       uint64_t* __restrict__ perm, unsigned* flags) {
+// Validate a chunk of host-order nonzeros, store 32-bit local coordinates and
+// the value in T, and form the mixed-radix block key
+// ((c_1 b_2 + c_2) b_3 + ...) b_d + c_d with c = i - lo.
+template <typename T, typename PermT>
+__global__ void k_convert(const KeyArgs ka, int64_t base, int64_t n, const int64_t* __restrict__ subs,
+                          const double* __restrict__ vals, uint32_t* __restrict__ coords, T* __restrict__ valt,
+                          uint64_t* __restrict__ klo, uint64_t* __restrict__ khi, PermT* __restrict__ perm,
+                          unsigned* flags) {
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gx = base + x;
         unsigned __int128 key = 0;
         unsigned bad = 0;
         for (int k = 0; k < ka.d; ++k) {
             const int64_t i = subs[x * ka.d + k];
-            if (i < ka.lo[k] || i >= ka.hi[k]) { bad |= BAD_RANGE; break; }
-            key = key * ka.bdim[k] + (uint64_t)(i - ka.lo[k]);
+            if (i < ka.lo[k] || i >= ka.hi[k]) {
+                bad |= BAD_RANGE;
+                coords[gx * ka.d + k] = 0;
+                continue;
+            }
+            const uint64_t c = (uint64_t)(i - ka.lo[k]);
+            coords[gx * ka.d + k] = (uint32_t)c;
+            key = key * ka.bdim[k] + c;
         }
-        if (!isfinite(vals[x])) bad |= BAD_VALUE;
+        const double v = vals[x];
+        if (!isfinite(v)) bad |= BAD_VALUE;
         if (bad) atomicOr(flags, bad);
-        klo[x] = (uint64_t)key;
-        if (khi) khi[x] = (uint64_t)(key >> 64);
-        perm[x] = (uint64_t)x;
+        valt[gx] = (T)v;
+        klo[gx] = (uint64_t)key;
+        if (khi) khi[gx] = (uint64_t)(key >> 64);
+        perm[gx] = (PermT)gx;
     }
 }
 
-__global__ void k_gather_hi(int64_t n, const uint64_t* __restrict__ perm, const uint64_t* __restrict__ hi_in,
-                            uint64_t* __restrict__ hi_out) {
+template <typename PermT>
+__global__ void k_gather_u64(int64_t n, const PermT* __restrict__ perm, const uint64_t* __restrict__ in,
+                             uint64_t* __restrict__ out) {
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
-        hi_out[x] = hi_in[perm[x]];
+        out[x] = in[perm[x]];
 }
 
-__global__ void k_gather_lo(int64_t n, const uint64_t* __restrict__ perm, const uint64_t* __restrict__ lo_in,
-                            uint64_t* __restrict__ lo_out) {
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
-        lo_out[x] = lo_in[perm[x]];
+// keys of the canonical order, recomputed from the local coordinates
+template <typename PermT>
+__global__ void k_sorted_keys(const KeyArgs ka, int64_t n, const PermT* __restrict__ perm,
+                              const uint32_t* __restrict__ coords, uint64_t* __restrict__ klo,
+                              uint64_t* __restrict__ khi) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t src = (int64_t)perm[x];
+        unsigned __int128 key = 0;
+        for (int k = 0; k < ka.d; ++k) key = key * ka.bdim[k] + coords[src * ka.d + k];
+        klo[x] = (uint64_t)key;
+        if (khi) khi[x] = (uint64_t)(key >> 64);
+    }
 }
 
 __global__ void k_dupcheck(int64_t n, const uint64_t* __restrict__ klo, const uint64_t* __restrict__ khi,
@@ -59,16 +87,16 @@ __global__ void k_dupcheck(int64_t n, const uint64_t* __restrict__ klo, const ui
 }
 
 // Canonical AoS record n = [value][local coords][pad] of nonzero perm[n].
-template <typename T>
-__global__ void k_records(int d, int64_t n, int rec_words, int val_words, const KeyArgs ka,
-                          const uint64_t* __restrict__ perm, const int64_t* __restrict__ subs,
-                          const double* __restrict__ vals, uint32_t* __restrict__ rec) {
+template <typename T, typename PermT>
+__global__ void k_records(int d, int64_t n, int rec_words, const PermT* __restrict__ perm,
+                          const uint32_t* __restrict__ coords, const T* __restrict__ valt, uint32_t* __restrict__ rec) {
+    constexpr int VW = (int)(sizeof(T) / 4);
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t src = (int64_t)perm[x];
         uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const T v = (T)vals[src];
+        const T v = valt[src];
         memcpy(w, &v, sizeof(T));
-        for (int k = 0; k < d; ++k) w[val_words + k] = (uint32_t)(subs[src * d + k] - ka.lo[k]);
+        for (int k = 0; k < d; ++k) w[VW + k] = coords[src * d + k];
         uint4* dst = reinterpret_cast<uint4*>(rec + x * rec_words);
         dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
         if (rec_words == 8) dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -156,133 +184,147 @@ cudaError_t launch_contains(gcp_ctx* c, int64_t n, const int64_t* coords, int8_t
     return cudaGetLastError();
 }
 
+
 #define CK(x)                                              \
     do {                                                   \
         cudaError_t e_ = (x);                              \
         if (e_ != cudaSuccess) { err = e_; goto cleanup; } \
     } while (0)
 
-gcp_status ingest(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h, const double* vals_h) {
-    // g: staged geometry (d, lo, hi, M) of the new tensor; c: the context (stream, scratch)
+template <typename T, typename PermT>
+static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h,
+                              const double* vals_h) {
     const KeyArgs ka = key_args(g);
     const int d = g->d;
     cudaStream_t st = c->stream;
     cudaError_t err = cudaSuccess;
     gcp_status status = GCP_OK;
-    int64_t* d_subs = nullptr;
-    double* d_vals = nullptr;
-    uint64_t *k0 = nullptr, *k1 = nullptr, *p0 = nullptr, *p1 = nullptr, *hi0 = nullptr, *hi1 = nullptr;
-    unsigned* d_flags = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
-    unsigned flags = 0;
-    const int nb = (int)std::min<int64_t>(std::max<int64_t>((nnz + 255) / 256, 1), (int64_t)c->sm_count * 16);
     const int kbits = bits_for(g->M > 0 ? g->M : 1);
     const bool k128 = kbits > 64;
-    const uint64_t slots_needed = (uint64_t)std::ceil((double)(nnz > 0 ? nnz : 1) / kHashLoad);
+    const bool sorted_member = c->member == GCP_MEMBER_SORTED;
+    const int rec_words = ((int)(sizeof(T) / 4) + d <= 4) ? 4 : 8;
+    const int nb = (int)std::min<int64_t>(std::max<int64_t>((nnz + 255) / 256, 1), (int64_t)c->sm_count * 16);
+    const int64_t chunk = std::min<int64_t>(std::max<int64_t>(nnz, 1), (int64_t)1 << 26);
     uint64_t slots = 4;
-    while (slots < slots_needed) slots <<= 1;
-    const int tw = (c->prec == GCP_FP32) ? 4 : 8;
-
+    if (!sorted_member) {
+        const uint64_t need = (uint64_t)std::ceil((double)std::max<int64_t>(nnz, 1) / kHashLoad);
+        while (slots < need) slots <<= 1;
+    }
+    const size_t kw = k128 ? 2 : 1;   // key words
+    unsigned flags = 0;
+    unsigned* d_flags = nullptr;
+    int64_t* d_sc = nullptr;
+    double* d_vc = nullptr;
+    uint32_t* coords = nullptr;
+    T* valt = nullptr;
+    uint64_t *k0 = nullptr, *k1 = nullptr, *h0 = nullptr, *h1 = nullptr;
+    PermT *p0 = nullptr, *p1 = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    PermT* perm = nullptr;
+    uint64_t *skl = nullptr, *skh = nullptr;
     uint32_t* new_rec = nullptr;
     uint64_t* new_hash = nullptr;
     uint64_t* new_keys = nullptr;
-    const bool sorted_member = c->member == GCP_MEMBER_SORTED;
-    const int val_words = tw / 4;
-    const int rec_words = (val_words + d <= 4) ? 4 : 8;
-    if (sorted_member) slots = 4;   // no hash set: a 4-slot empty table keeps the pointer valid
 
     CK(cudaMalloc(&d_flags, sizeof(unsigned)));
     CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
-    CK(cudaMalloc(&new_rec, (size_t)std::max<int64_t>(nnz, 1) * rec_words * 4));
-    CK(cudaMalloc(&new_hash, (size_t)slots * 8 * (k128 ? 2 : 1)));
-    CK(cudaMemsetAsync(new_hash, 0xFF, (size_t)slots * 8 * (k128 ? 2 : 1), st));
-    CK(cudaMalloc(&new_keys, (size_t)(sorted_member ? std::max<int64_t>(nnz, 1) : 1) * 8 * (k128 ? 2 : 1)));
     if (nnz > 0) {
-        CK(cudaMalloc(&d_subs, (size_t)nnz * d * sizeof(int64_t)));
-        CK(cudaMalloc(&d_vals, (size_t)nnz * sizeof(double)));
-        CK(cudaMemcpyAsync(d_subs, subs_h, (size_t)nnz * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d_vals, vals_h, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+        // 1) stream the host COO through the staging buffer, converting on the fly
+        CK(cudaMalloc(&coords, (size_t)nnz * d * 4));
+        CK(cudaMalloc(&valt, (size_t)nnz * sizeof(T)));
         CK(cudaMalloc(&k0, (size_t)nnz * 8));
-        CK(cudaMalloc(&k1, (size_t)nnz * 8));
-        CK(cudaMalloc(&p0, (size_t)nnz * 8));
-        CK(cudaMalloc(&p1, (size_t)nnz * 8));
-        if (k128) {
-            CK(cudaMalloc(&hi0, (size_t)nnz * 8));
-            CK(cudaMalloc(&hi1, (size_t)nnz * 8));
+        if (k128) CK(cudaMalloc(&h0, (size_t)nnz * 8));
+        CK(cudaMalloc(&p0, (size_t)nnz * sizeof(PermT)));
+        CK(cudaMalloc(&d_sc, (size_t)chunk * d * 8));
+        CK(cudaMalloc(&d_vc, (size_t)chunk * 8));
+        for (int64_t b = 0; b < nnz; b += chunk) {
+            const int64_t n = std::min(chunk, nnz - b);
+            CK(cudaMemcpyAsync(d_sc, subs_h + b * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_vc, vals_h + b, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+            k_convert<T, PermT><<<nb, 256, 0, st>>>(ka, b, n, d_sc, d_vc, coords, valt, k0, h0, p0, d_flags);
+            CK(cudaGetLastError());
+            c->launches++;
         }
-        k_keys<<<nb, 256, 0, st>>>(ka, nnz, d_subs, d_vals, k0, hi0, p0, d_flags);
-        CK(cudaGetLastError());
-        c->launches++;
         CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        cudaFree(d_sc); d_sc = nullptr;
+        cudaFree(d_vc); d_vc = nullptr;
         if (flags & BAD_RANGE) { status = set_error(GCP_E_RANGE, "gcp_tensor_create: coordinate outside dims / block"); goto cleanup; }
         if (flags & BAD_VALUE) { status = set_error(GCP_E_ARG, "gcp_tensor_create: non-finite value"); goto cleanup; }
+        // 2) LSD radix sort of (key, perm): low word, then stably the high word
+        CK(cudaMalloc(&k1, (size_t)nnz * 8));
+        CK(cudaMalloc(&p1, (size_t)nnz * sizeof(PermT)));
         {
-            // LSD radix sort: (low 64 bits, perm), then stably by the high word
-            cub::DoubleBuffer<uint64_t> keys(k0, k1), perm(p0, p1);
-            const int lo_bits = k128 ? 64 : (kbits > 0 ? kbits : 1);
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, perm, nnz, 0, lo_bits, st));
+            cub::DoubleBuffer<uint64_t> keys(k0, k1);
+            cub::DoubleBuffer<PermT> pm(p0, p1);
+            const int lo_bits = k128 ? 64 : std::max(kbits, 1);
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, pm, nnz, 0, lo_bits, st));
             CK(cudaMalloc(&tmp, tmp_bytes));
-            CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, perm, nnz, 0, lo_bits, st));
-            uint64_t* sorted_lo = keys.Current();
-            uint64_t* sorted_perm = perm.Current();
-            uint64_t* sorted_hi = nullptr;
+            CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, pm, nnz, 0, lo_bits, st));
             if (k128) {
-                // hi' = hi[perm]; sort (hi', perm) stably; then lo = key_lo[perm]
-                uint64_t* other_perm = perm.Alternate();
-                k_gather_hi<<<nb, 256, 0, st>>>(nnz, sorted_perm, hi0, hi1);
+                // high words in the current order, then a stable sort on them
+                uint64_t* hbuf = keys.Alternate();
+                k_gather_u64<PermT><<<nb, 256, 0, st>>>(nnz, pm.Current(), h0, hbuf);
                 CK(cudaGetLastError());
                 c->launches++;
-                cub::DoubleBuffer<uint64_t> hk(hi1, hi0), pp(sorted_perm, other_perm);
+                cub::DoubleBuffer<uint64_t> hk(hbuf, keys.Current());
                 size_t tb2 = 0;
-                CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hk, pp, nnz, 0, kbits - 64, st));
+                CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hk, pm, nnz, 0, kbits - 64, st));
                 if (tb2 > tmp_bytes) {
                     cudaFree(tmp);
                     tmp = nullptr;
                     CK(cudaMalloc(&tmp, tb2));
                     tmp_bytes = tb2;
                 }
-                CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, hk, pp, nnz, 0, kbits - 64, st));
-                sorted_hi = hk.Current();
-                sorted_perm = pp.Current();
-                // recompute low words in the final order from the original keys
-                uint64_t* lo_orig = (sorted_lo == k0) ? k1 : k0;   // scratch
-                k_keys<<<nb, 256, 0, st>>>(ka, nnz, d_subs, d_vals, lo_orig, hk.Alternate(), pp.Alternate(),
-                                           d_flags);
-                CK(cudaGetLastError());
-                c->launches++;
-                k_gather_lo<<<nb, 256, 0, st>>>(nnz, sorted_perm, lo_orig, sorted_lo);
-                CK(cudaGetLastError());
-                c->launches++;
+                CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, hk, pm, nnz, 0, kbits - 64, st));
             }
-            k_dupcheck<<<nb, 256, 0, st>>>(nnz, sorted_lo, sorted_hi, d_flags);
+            perm = pm.Current();
+            // keys in canonical order, recomputed from the coordinates into the
+            // (now free) key buffers
+            skl = k0;
+            skh = k128 ? h0 : nullptr;
+            k_sorted_keys<PermT><<<nb, 256, 0, st>>>(ka, nnz, perm, coords, skl, skh);
             CK(cudaGetLastError());
             c->launches++;
-            if (c->prec == GCP_FP32)
-                k_records<float><<<nb, 256, 0, st>>>(d, nnz, rec_words, val_words, ka, sorted_perm, d_subs,
-                                                     d_vals, new_rec);
-            else
-                k_records<double><<<nb, 256, 0, st>>>(d, nnz, rec_words, val_words, ka, sorted_perm, d_subs,
-                                                      d_vals, new_rec);
-            CK(cudaGetLastError());
-            c->launches++;
-            if (sorted_member)
-                k_store_keys<<<nb, 256, 0, st>>>(nnz, sorted_lo, sorted_hi, new_keys);
-            else
-                k_hash_insert<<<nb, 256, 0, st>>>(nnz, sorted_lo, sorted_hi, new_hash, slots - 1);
-            CK(cudaGetLastError());
-            c->launches++;
-            CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (flags & BAD_DUP) { status = set_error(GCP_E_DUP, "gcp_tensor_create: duplicate coordinates"); goto cleanup; }
         }
+        cudaFree(tmp); tmp = nullptr;
+        cudaFree(k1); k1 = nullptr;
+        cudaFree(perm == p0 ? p1 : p0);
+        if (perm == p0) p1 = nullptr; else p0 = nullptr;
+        // 3) duplicates, records
+        k_dupcheck<<<nb, 256, 0, st>>>(nnz, skl, skh, d_flags);
+        CK(cudaGetLastError());
+        c->launches++;
+        CK(cudaMalloc(&new_rec, (size_t)nnz * rec_words * 4));
+        k_records<T, PermT><<<nb, 256, 0, st>>>(d, nnz, rec_words, perm, coords, valt, new_rec);
+        CK(cudaGetLastError());
+        c->launches++;
+        CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (flags & BAD_DUP) { status = set_error(GCP_E_DUP, "gcp_tensor_create: duplicate coordinates"); goto cleanup; }
+        cudaFree(coords); coords = nullptr;
+        cudaFree(valt); valt = nullptr;
+        cudaFree(p0); p0 = nullptr;
+        cudaFree(p1); p1 = nullptr;
+    } else {
+        CK(cudaMalloc(&new_rec, (size_t)rec_words * 4));
+    }
+    // 4) zero-test structure
+    CK(cudaMalloc(&new_hash, (size_t)slots * 8 * kw));
+    CK(cudaMemsetAsync(new_hash, 0xFF, (size_t)slots * 8 * kw, st));
+    CK(cudaMalloc(&new_keys, (size_t)(sorted_member ? std::max<int64_t>(nnz, 1) : 1) * 8 * kw));
+    if (nnz > 0) {
+        if (sorted_member) k_store_keys<<<nb, 256, 0, st>>>(nnz, skl, skh, new_keys);
+        else k_hash_insert<<<nb, 256, 0, st>>>(nnz, skl, skh, new_hash, slots - 1);
+        CK(cudaGetLastError());
+        c->launches++;
     }
     CK(cudaStreamSynchronize(st));
 
 cleanup:
-    cudaFree(d_subs); cudaFree(d_vals); cudaFree(k0); cudaFree(k1); cudaFree(p0); cudaFree(p1);
-    cudaFree(hi0); cudaFree(hi1); cudaFree(tmp); cudaFree(d_flags);
+    cudaFree(d_flags); cudaFree(d_sc); cudaFree(d_vc); cudaFree(coords); cudaFree(valt);
+    cudaFree(k0); cudaFree(k1); cudaFree(h0); cudaFree(h1); cudaFree(p0); cudaFree(p1); cudaFree(tmp);
     if (err != cudaSuccess || status != GCP_OK) {
         cudaFree(new_rec);
         cudaFree(new_hash);
@@ -302,10 +344,19 @@ cleanup:
     c->d_hash = new_hash;
     c->d_keys = new_keys;
     c->key128 = k128 ? 1 : 0;
-    c->val_words = val_words;
+    c->val_words = (int)(sizeof(T) / 4);
     c->rec_words = rec_words;
     c->hash_slots = slots;
     return GCP_OK;
+}
+
+gcp_status ingest(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h, const double* vals_h) {
+    const bool p32 = nnz < ((int64_t)1 << 32);
+    if (c->prec == GCP_FP32)
+        return p32 ? ingest_impl<float, uint32_t>(c, g, nnz, subs_h, vals_h)
+                   : ingest_impl<float, uint64_t>(c, g, nnz, subs_h, vals_h);
+    return p32 ? ingest_impl<double, uint32_t>(c, g, nnz, subs_h, vals_h)
+               : ingest_impl<double, uint64_t>(c, g, nnz, subs_h, vals_h);
 }
 
 }  // namespace gcp

@@ -25,12 +25,16 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--l2fetch", default="", help="comma list of cudaLimitMaxL2FetchGranularity values to sweep")
     args = ap.parse_args()
     import paper_2605_20353_b200 as g
     c = gcp_synth.CONFIGS[args.config]
     s = gcp_synth.SEEDS[args.config]
     subs, vals = gcp_synth.chi_kolda(c["dims"], c["nnz"], c["R"], s["data"], c["loss"], device="cuda")
-    subs_h, vals_h = subs.cpu().pin_memory(), vals.cpu().pin_memory()
+    subs_h = torch.empty(subs.shape, dtype=subs.dtype, pin_memory=True)
+    subs_h.copy_(subs)
+    vals_h = torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True)
+    vals_h.copy_(vals)
     del subs, vals
     torch.cuda.empty_cache()
     stream = torch.cuda.Stream()
@@ -44,20 +48,27 @@ def main():
         ctx.loss_grad(c["loss"])
         ctx.adam_step()
     ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
-    ctx.profile_enable(True)
-    for k in ("grad", "adam", "loss", "other"):
-        ctx.profile_get(k, reset=True)
-    for _ in range(args.iters):
-        ctx.loss_grad(c["loss"])
-        ctx.adam_step()
-    for _ in range(3):
-        ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
-    out = {"config": args.config, "L2_FETCH": os.environ.get("GCP_L2_FETCH", "default(32)"), "ingest_s": t_ingest}
-    for k in ("grad", "adam", "loss"):
-        ms, n = ctx.profile_get(k)
-        out[k + "_ms"] = ms / max(n, 1)
-    out["samples_per_s_k2"] = 2 * c["s"] / (out["grad_ms"] * 1e-3)
-    print(json.dumps(out), flush=True)
+    sweep = [int(x) for x in args.l2fetch.split(",")] if args.l2fetch else [None]
+    for l2f in sweep:
+        if l2f is not None:   # device-wide hint through the process's CUDA runtime
+            import ctypes
+            rt = ctypes.CDLL("libcudart.so.12")
+            rt.cudaDeviceSetLimit(ctypes.c_int(0x05), ctypes.c_size_t(l2f))   # cudaLimitMaxL2FetchGranularity
+        ctx.profile_enable(True)
+        for k in ("grad", "adam", "loss", "other"):
+            ctx.profile_get(k, reset=True)
+        for _ in range(args.iters):
+            ctx.loss_grad(c["loss"])
+            ctx.adam_step()
+        for _ in range(3):
+            ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
+        out = {"config": args.config, "L2_FETCH": l2f if l2f is not None else os.environ.get("GCP_L2_FETCH", "32"),
+               "ingest_s": t_ingest}
+        for k in ("grad", "adam", "loss"):
+            ms, n = ctx.profile_get(k)
+            out[k + "_ms"] = ms / max(n, 1)
+        out["samples_per_s_k2"] = 2 * c["s"] / (out["grad_ms"] * 1e-3)
+        print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
