@@ -119,6 +119,8 @@ double u128_to_double(unsigned __int128 v) { return (double)v; }
 double loss_lower(int loss) { return loss == GCP_LOSS_POISSON ? 0.0 : -INFINITY; }
 
 void free_model(gcp_ctx* c) {
+    if (c->ag_interleaved) c->d_G = nullptr;   // a view into d_A
+    c->ag_interleaved = false;
     void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C, &c->d_lambda, &c->d_Ack, &c->d_Bck, &c->d_Cck,
                      &c->d_U,  &c->d_Bs, &c->d_Cs};
     for (void** b : bufs) {
@@ -172,8 +174,10 @@ ModelArgs model_args(const gcp_ctx* c) {
     m.A = c->d_A;
     m.G = c->d_G;
     m.lambda = c->d_lambda;
-    for (int k = 0; k < kMaxModes; ++k) m.off[k] = k < c->d ? c->off[k] : 0;
+    const int64_t mult = c->ag_stride / c->R_pad;   // 1, or 2 when A/G rows interleave
+    for (int k = 0; k < kMaxModes; ++k) m.off[k] = k < c->d ? c->off[k] * mult : 0;
     m.R_pad = c->R_pad;
+    m.row_stride = c->ag_stride;
     return m;
 }
 
@@ -223,14 +227,21 @@ gcp_status run_loss_kernel(gcp_ctx* c, int loss, int64_t p, int64_t q, uint64_t 
 
 size_t tsz(const gcp_ctx* c) { return c->prec == GCP_FP32 ? 4 : 8; }
 
+// element offset of mode k's first row in the A (or G) buffer
+int64_t phys_off(const gcp_ctx* c, int k) { return c->off[k] * (c->ag_stride / c->R_pad); }
+
+// elements of the A allocation (twice n_coef when G rows are interleaved into it)
+size_t a_elems(const gcp_ctx* c) { return (size_t)c->n_coef * (c->ag_interleaved ? 2 : 1); }
+
 gcp_status checkpoint_save(gcp_ctx* c) {
     const size_t bytes = (size_t)c->n_coef * tsz(c);
+    const size_t abytes = a_elems(c) * tsz(c);   // A (with interleaved G rows, which are zero here)
     if (!c->d_Ack) {
-        CUDA_TRY(c, cudaMalloc(&c->d_Ack, bytes), "checkpoint alloc");
+        CUDA_TRY(c, cudaMalloc(&c->d_Ack, abytes), "checkpoint alloc");
         CUDA_TRY(c, cudaMalloc(&c->d_Bck, bytes), "checkpoint alloc");
         CUDA_TRY(c, cudaMalloc(&c->d_Cck, bytes), "checkpoint alloc");
     }
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_Ack, c->d_A, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_Ack, c->d_A, abytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
     CUDA_TRY(c, cudaMemcpyAsync(c->d_Bck, c->d_B, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
     CUDA_TRY(c, cudaMemcpyAsync(c->d_Cck, c->d_C, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
     c->t_ck = c->t;
@@ -240,10 +251,11 @@ gcp_status checkpoint_save(gcp_ctx* c) {
 
 gcp_status checkpoint_restore(gcp_ctx* c) {
     const size_t bytes = (size_t)c->n_coef * tsz(c);
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_A, c->d_Ack, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
+    const size_t abytes = a_elems(c) * tsz(c);
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_A, c->d_Ack, abytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
     CUDA_TRY(c, cudaMemcpyAsync(c->d_B, c->d_Bck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
     CUDA_TRY(c, cudaMemcpyAsync(c->d_C, c->d_Cck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
-    CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "restore");
+    if (!c->ag_interleaved) CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "restore");
     c->t = c->t_ck;
     c->ts = c->ts_ck;
     return GCP_OK;
@@ -300,6 +312,7 @@ gcp_status gcp_create(gcp_ctx** out, int cuda_device, void* cuda_stream, gcp_pre
     c->prec = prec;
     c->tsize = prec == GCP_FP32 ? 4 : 8;
     c->sm_count = prop.multiProcessorCount;
+    c->l2_bytes = prop.l2CacheSize;
     if (cudaMallocHost(&c->h_scalar, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess ||
         cudaMalloc(&c->d_err, 64) != cudaSuccess) {
         gcp_destroy(c);
@@ -526,18 +539,49 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
             c->ar_mode[k] = pol == "ar" || (pol == "auto" && mb <= 16.0);
         }
     }
+    {
+        // A/G row interleaving: with one rank in sync mode and a row pair that
+        // tiles a 128-B line (R_pad*sizeof(T) in {16, 32, 64}), row i of A^(k)
+        // and of G^(k) share one line, so K2's scatter-add hits the line its
+        // gather just filled (DRAM traffic per sampled row: 1 fill + 1 write-back
+        // instead of 2 fills + 1 write-back).  GCP_AG_INTERLEAVE=0/1 overrides.
+        // Only when A + G spill out of L2: with L2-resident factors (c2) the
+        // gathers and scatter-adds sharing lines contend in the L2 slices and
+        // K2 is ~20% slower; for DRAM-resident factors (c4) it is ~20% faster.
+        const size_t rb = (size_t)c->R_pad * tsz(c);
+        const bool spills = 2.0 * (double)c->n_coef * (double)tsz(c) > 0.5 * (double)c->l2_bytes;
+        bool il = c->P == 1 && c->mode == GCP_DIST_SYNC && (rb == 16 || rb == 32 || rb == 64) && spills;
+        const char* env = getenv("GCP_AG_INTERLEAVE");
+        if (env) il = atoi(env) != 0 && c->P == 1 && c->mode == GCP_DIST_SYNC;
+        c->ag_interleaved = il;
+        c->ag_stride = il ? 2 * c->R_pad : c->R_pad;
+    }
     const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
-    void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C};
-    for (void** b : bufs) {
-        cudaError_t e = cudaMalloc(b, bytes);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            free_model(c);
-            return set_error(GCP_E_OOM, "gcp_model_init: out of device memory");
+    {
+        void** bufs[] = {&c->d_A, &c->d_B, &c->d_C};
+        for (void** b : bufs) {
+            cudaError_t e = cudaMalloc(b, b == &c->d_A && c->ag_interleaved ? 2 * bytes : bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                free_model(c);
+                return set_error(GCP_E_OOM, "gcp_model_init: out of device memory");
+            }
+        }
+        if (c->ag_interleaved) {
+            c->d_G = (char*)c->d_A + (size_t)c->R_pad * tsz(c);   // view: G rows interleaved with A rows
+        } else {
+            cudaError_t e = cudaMalloc(&c->d_G, bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                free_model(c);
+                return set_error(GCP_E_OOM, "gcp_model_init: out of device memory");
+            }
         }
     }
     CUDA_TRY(c, cudaMalloc(&c->d_lambda, (size_t)c->R_pad * tsz(c)), "model lambda");
-    CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "model init");
+    CUDA_TRY(c, cudaMemsetAsync(c->ag_interleaved ? c->d_A : c->d_G, 0, c->ag_interleaved ? 2 * bytes : bytes,
+                                c->stream),
+             "model init");
     CUDA_TRY(c, cudaMemsetAsync(c->d_B, 0, bytes, c->stream), "model init");
     CUDA_TRY(c, cudaMemsetAsync(c->d_C, 0, bytes, c->stream), "model init");
     {
@@ -580,14 +624,18 @@ gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* la
         std::vector<float> h(n, 0.f);
         for (int64_t i = 0; i < b; ++i)
             for (int r = 0; r < c->R; ++r) h[(size_t)i * c->R_pad + r] = (float)rows[i * c->R + r];
-        CUDA_TRY(c, cudaMemcpyAsync((float*)c->d_A + c->off[k], h.data(), n * 4, cudaMemcpyHostToDevice, c->stream),
+        CUDA_TRY(c, cudaMemcpy2DAsync((float*)c->d_A + phys_off(c, k), (size_t)c->ag_stride * 4, h.data(),
+                                      (size_t)c->R_pad * 4, (size_t)c->R_pad * 4, (size_t)b, cudaMemcpyHostToDevice,
+                                      c->stream),
                  "model_set");
         CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
     } else {
         std::vector<double> h(n, 0.0);
         for (int64_t i = 0; i < b; ++i)
             for (int r = 0; r < c->R; ++r) h[(size_t)i * c->R_pad + r] = rows[i * c->R + r];
-        CUDA_TRY(c, cudaMemcpyAsync((double*)c->d_A + c->off[k], h.data(), n * 8, cudaMemcpyHostToDevice, c->stream),
+        CUDA_TRY(c, cudaMemcpy2DAsync((double*)c->d_A + phys_off(c, k), (size_t)c->ag_stride * 8, h.data(),
+                                      (size_t)c->R_pad * 8, (size_t)c->R_pad * 8, (size_t)b, cudaMemcpyHostToDevice,
+                                      c->stream),
                  "model_set");
         CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
     }
@@ -606,20 +654,25 @@ gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* la
     return server_reset(c);   // FedAdam: the server copy starts from the model as set
 }
 
+// rows of A or G (row stride ag_stride) of mode k's block to a packed R_pad-wide host copy
 static gcp_status read_rows(gcp_ctx* c, const void* base, int k, double* out, const char* what) {
     const int64_t b = c->hi[k] - c->lo[k];
     const size_t n = (size_t)b * c->R_pad;
+    const size_t ts = tsz(c);
     if (c->prec == GCP_FP32) {
         std::vector<float> h(n);
-        CUDA_TRY(c, cudaMemcpyAsync(h.data(), (const float*)base + c->off[k], n * 4, cudaMemcpyDeviceToHost, c->stream),
+        CUDA_TRY(c, cudaMemcpy2DAsync(h.data(), (size_t)c->R_pad * ts, (const float*)base + phys_off(c, k),
+                                      (size_t)c->ag_stride * ts, (size_t)c->R_pad * ts, (size_t)b,
+                                      cudaMemcpyDeviceToHost, c->stream),
                  what);
         CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
         for (int64_t i = 0; i < b; ++i)
             for (int r = 0; r < c->R; ++r) out[i * c->R + r] = h[(size_t)i * c->R_pad + r];
     } else {
         std::vector<double> h(n);
-        CUDA_TRY(c, cudaMemcpyAsync(h.data(), (const double*)base + c->off[k], n * 8, cudaMemcpyDeviceToHost,
-                                    c->stream),
+        CUDA_TRY(c, cudaMemcpy2DAsync(h.data(), (size_t)c->R_pad * ts, (const double*)base + phys_off(c, k),
+                                      (size_t)c->ag_stride * ts, (size_t)c->R_pad * ts, (size_t)b,
+                                      cudaMemcpyDeviceToHost, c->stream),
                  what);
         CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
         for (int64_t i = 0; i < b; ++i)
@@ -774,7 +827,7 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     cudaEvent_t ev;
     prof_begin(c, PROF_ADAM, &ev);
     CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower, c->t,
-                            sharded ? 0 : 1),
+                            sharded ? 0 : 1, c->ag_stride),
              "gcp_adam_step");
     prof_end(c, PROF_ADAM, ev);
     if (sharded) {

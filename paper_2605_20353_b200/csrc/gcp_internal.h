@@ -56,8 +56,9 @@ struct ModelArgs {
     const void* A;            // factor array (T), mode-major, rows padded to R_pad
     void* G;                  // gradient array, same layout
     const void* lambda;       // R_pad values (T), zero padded
-    int64_t off[kMaxModes];   // element offset of mode k
+    int64_t off[kMaxModes];   // element offset of mode k's first row in the A (and G) buffer
     int R_pad;
+    int row_stride;           // elements between consecutive rows (R_pad, or 2 R_pad when A/G interleave)
 };
 
 struct Segment {              // contiguous ranges of the coefficient arrays (Adam)
@@ -73,6 +74,7 @@ struct gcp_ctx {
     cudaStream_t stream = nullptr;
     gcp_precision prec = GCP_FP32;
     int sm_count = 148;
+    int64_t l2_bytes = 126 << 20;
     int tsize = 4;                      // sizeof(T)
     // ---- error state
     gcp_status sticky = GCP_OK;
@@ -108,7 +110,9 @@ struct gcp_ctx {
     int R = 0, R_pad = 0;
     int64_t rows[gcp::kMaxModes] = {0};     // allocated rows per mode (>= block rows, multiple of slice size)
     int64_t off[gcp::kMaxModes] = {0};      // element offsets
-    int64_t n_coef = 0;
+    int64_t n_coef = 0;                     // logical coefficients (B, C layout)
+    bool ag_interleaved = false;            // A and G rows interleaved in one buffer (d_G = d_A + R_pad)
+    int ag_stride = 0;                      // elements between consecutive A (or G) rows
     void *d_A = nullptr, *d_G = nullptr, *d_B = nullptr, *d_C = nullptr, *d_lambda = nullptr;
     void *d_Ack = nullptr, *d_Bck = nullptr, *d_Cck = nullptr;   // fit checkpoint
     void *d_U = nullptr, *d_Bs = nullptr, *d_Cs = nullptr;       // FedAdam server copy + state
@@ -163,7 +167,7 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C,
                         double rate, double beta1, double beta2, double eps, double lower,
-                        int64_t t, int zero_g);
+                        int64_t t, int zero_g, int row_stride = 0);   // row_stride 0: contiguous A/G
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
 cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);

@@ -15,9 +15,9 @@ cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int6
 cudaError_t export_f64(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
                        int32_t*);
 cudaError_t adam_f32(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int);
+                     double, int64_t, int, int, int);
 cudaError_t adam_f64(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int);
+                     double, int64_t, int, int, int);
 cudaError_t init_f32(gcp_ctx*, const InitArgs&, void*);
 cudaError_t init_f64(gcp_ctx*, const InitArgs&, void*);
 
@@ -42,14 +42,17 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
 }
 
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
-                        double beta1, double beta2, double eps, double lower, int64_t t, int zero_g) {
-    return c->prec == GCP_FP32 ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g)
-                               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g);
+                        double beta1, double beta2, double eps, double lower, int64_t t, int zero_g,
+                        int row_stride) {
+    const int rs = row_stride > 0 ? row_stride : c->R_pad;
+    return c->prec == GCP_FP32 ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs)
+                               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs);
 }
 
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
     InitArgs ia;
-    ia.d = c->d; ia.R = c->R; ia.R_pad = c->R_pad; ia.n_coef = c->n_coef; ia.seed = seed;
+    ia.d = c->d; ia.R = c->R; ia.R_pad = c->R_pad; ia.row_stride = c->ag_stride; ia.n_coef = c->n_coef;
+    ia.seed = seed;
     for (int k = 0; k < kMaxModes; ++k) {
         ia.rows[k] = k < c->d ? c->rows[k] : 0;
         ia.bdim[k] = k < c->d ? c->hi[k] - c->lo[k] : 0;

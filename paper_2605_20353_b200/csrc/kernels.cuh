@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                 rf[b] = __shfl_sync(0xffffffffu, flags, src);
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    const T* row = A + ma.off[k] + (int64_t)rc[b][k] * R_pad;
+                    const T* row = A + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
                         if ((rf[b] & 1) && vok[v]) ldg_vec<T, VE>(a[b][k][v], row + (gl + v * GL) * VE);
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                 if (!kp.loss_mode && ok) {
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
-                        T* grow = G + ma.off[k] + (int64_t)rc[b][k] * R_pad;
+                        T* grow = G + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {
                             if (!vok[v]) continue;
@@ -228,7 +228,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
                                               T* __restrict__ G, T* __restrict__ B, T* __restrict__ C,
                                               T rate, T b1, T b2, T eps, T bc1, T bc2, T lower,
-                                              int zero_g) {
+                                              int zero_g, int R_pad, int row_stride) {
     using V = typename Vec16<T>::type;
     constexpr int VE = Vec16<T>::n;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec_total;
@@ -237,9 +237,10 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
         int64_t rem = i;
         int sidx = 0;
         while (sidx < seg.n - 1 && rem >= seg.len[sidx] / VE) { rem -= seg.len[sidx] / VE; ++sidx; }
-        const int64_t e = seg.start[sidx] + rem * VE;
-        V g = *reinterpret_cast<const V*>(G + e);
-        V a = *reinterpret_cast<const V*>(A + e);
+        const int64_t e = seg.start[sidx] + rem * VE;                   // B, C (logical) index
+        const int64_t ea = (e / R_pad) * row_stride + e % R_pad;          // A, G (row-strided) index
+        V g = *reinterpret_cast<const V*>(G + ea);
+        V a = *reinterpret_cast<const V*>(A + ea);
         V b = *reinterpret_cast<const V*>(B + e);
         V c = *reinterpret_cast<const V*>(C + e);
         T* gp = reinterpret_cast<T*>(&g);
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
             T av = ap[q] - rate * ((bp[q] * bc1) / sqrt(cp[q] * bc2 + eps));
             ap[q] = (av < lower) ? lower : av;
         }
-        *reinterpret_cast<V*>(A + e) = a;
+        *reinterpret_cast<V*>(A + ea) = a;
         *reinterpret_cast<V*>(B + e) = b;
         *reinterpret_cast<V*>(C + e) = c;
         if (zero_g) {
@@ -262,13 +263,13 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
             T* zp = reinterpret_cast<T*>(&z);
 #pragma unroll
             for (int q = 0; q < VE; ++q) zp[q] = T(0);
-            *reinterpret_cast<V*>(G + e) = z;
+            *reinterpret_cast<V*>(G + ea) = z;
         }
     }
 }
 
 struct InitArgs {
-    int d, R, R_pad;
+    int d, R, R_pad, row_stride;
     int64_t rows[kMaxModes], bdim[kMaxModes], lo[kMaxModes], off[kMaxModes], goff[kMaxModes];
     int64_t n_coef;
     uint64_t seed;
@@ -292,7 +293,7 @@ __global__ void k_init(const InitArgs ia, T* __restrict__ A) {
                                    (uint32_t)ia.seed, (uint32_t)(ia.seed >> 32));
             v = (T)((double)(w.w0 >> 11) * 0x1.0p-53);
         }
-        A[x] = v;
+        A[(x / ia.R_pad) * ia.row_stride + x % ia.R_pad] = v;
     }
 }
 

@@ -123,6 +123,29 @@ def test_gradient_parity(gcp, orc, loss, strategy, prec):
     assert abs(ls - lo) <= TOL[prec] * max(1.0, abs(lo)) * 10
 
 
+@pytest.mark.parametrize("interleave", ["0", "1"])
+def test_ag_layouts_agree(gcp, orc, interleave, monkeypatch):
+    """Separate and row-interleaved A/G layouts: same gradient, same Adam step."""
+    monkeypatch.setenv("GCP_AG_INTERLEAVE", interleave)
+    dims = (20, 30, 40)
+    subs, vals = _tensor("gaussian")
+    c = _ctx(gcp, dims, subs, vals, prec="fp64")
+    t = orc.Tensor(dims, subs, vals)
+    c.sample("stratified", 700, 900, 3001)
+    A = _model(c, 3)
+    c.loss_grad("gaussian")
+    G = [c.grad_get(k) for k in range(3)]
+    Go, S, _ = orc.sampled_grad(t, A, "gaussian", 3001, 0, 0, 700, 900)
+    _grad_check(G, Go, S, 1e-10, f"interleave={interleave}")
+    c.adam_step(gcp.adam_params(rate=1e-2))
+    flat = np.concatenate([a.ravel() for a in A])
+    Gf = np.concatenate([g.ravel() for g in Go])
+    orc.adam(flat, Gf, np.zeros_like(flat), np.zeros_like(flat), 1, 1e-2, 0.9, 0.999, 1e-8)
+    got = np.concatenate([a.ravel() for a in _model(c, 3)])
+    assert np.allclose(got, flat, rtol=1e-9, atol=1e-12)
+    assert all((c.grad_get(k) == 0).all() for k in range(3))   # G reset fused into Adam
+
+
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
 @pytest.mark.parametrize("loss", LOSSES)
 def test_loss_estimate_parity(gcp, orc, loss, prec):
