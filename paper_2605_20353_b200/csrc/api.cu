@@ -119,6 +119,7 @@ double u128_to_double(unsigned __int128 v) { return (double)v; }
 double loss_lower(int loss) { return loss == GCP_LOSS_POISSON ? 0.0 : -INFINITY; }
 
 void free_model(gcp_ctx* c) {
+    fused_free(c);                             // symmetric A / G windows (collective)
     if (c->ag_interleaved) c->d_G = nullptr;   // a view into d_A
     c->ag_interleaved = false;
     void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C, &c->d_lambda, &c->d_Ack, &c->d_Bck, &c->d_Cck,
@@ -169,10 +170,14 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     return s;
 }
 
+// the G buffer the current iteration accumulates into (parity-double-buffered
+// under the fused exchange, fused.cu)
+void* cur_G(const gcp_ctx* c) { return (c->fused && (c->it & 1)) ? c->d_G2 : c->d_G; }
+
 ModelArgs model_args(const gcp_ctx* c) {
     ModelArgs m;
     m.A = c->d_A;
-    m.G = c->d_G;
+    m.G = cur_G(c);
     m.lambda = c->d_lambda;
     const int64_t mult = c->ag_stride / c->R_pad;   // 1, or 2 when A/G rows interleave
     for (int k = 0; k < kMaxModes; ++k) m.off[k] = k < c->d ? c->off[k] * mult : 0;
@@ -256,6 +261,7 @@ gcp_status checkpoint_restore(gcp_ctx* c) {
     CUDA_TRY(c, cudaMemcpyAsync(c->d_B, c->d_Bck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
     CUDA_TRY(c, cudaMemcpyAsync(c->d_C, c->d_Cck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
     if (!c->ag_interleaved) CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "restore");
+    if (c->fused) CUDA_TRY(c, cudaMemsetAsync(c->d_G2, 0, bytes, c->stream), "restore");
     c->t = c->t_ck;
     c->ts = c->ts_ck;
     return GCP_OK;
@@ -343,6 +349,7 @@ void gcp_destroy(gcp_ctx* c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (int k = 0; k < kMaxModes; ++k)
         if (c->slice[k]) ncclCommDestroy(c->slice[k]);
+    if (c->devcomm_ready) ncclDevCommDestroy(c->world, &c->devcomm);
     if (c->world) ncclCommDestroy(c->world);
     delete c;
 }
@@ -525,7 +532,10 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     for (int k = 0; k < c->d; ++k) {
         const int64_t b = c->hi[k] - c->lo[k];
         const int64_t g = (c->P > 1 && c->mode == GCP_DIST_SYNC) ? c->slice_size[k] : 1;
-        c->rows[k] = (b + g - 1) / g * g;
+        // sync P > 1: every rank uses the same padded layout (ceil block size,
+        // multiple of the slice size), so the A / G windows are symmetric
+        const int64_t cb = (c->P > 1 && c->mode == GCP_DIST_SYNC) ? (c->dims[k] + c->grid[k] - 1) / c->grid[k] : b;
+        c->rows[k] = (cb + g - 1) / g * g;
         c->off[k] = off;
         off += c->rows[k] * c->R_pad;
     }
@@ -557,9 +567,12 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         c->ag_stride = il ? 2 * c->R_pad : c->R_pad;
     }
     const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
+    const bool use_fused = fused_possible(c);
+    if (use_fused) ST_TRY(fused_alloc(c, bytes));   // A, G, G2: symmetric NVLink windows
     {
         void** bufs[] = {&c->d_A, &c->d_B, &c->d_C};
         for (void** b : bufs) {
+            if (use_fused && b == &c->d_A) continue;
             cudaError_t e = cudaMalloc(b, b == &c->d_A && c->ag_interleaved ? 2 * bytes : bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
@@ -569,6 +582,8 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         }
         if (c->ag_interleaved) {
             c->d_G = (char*)c->d_A + (size_t)c->R_pad * tsz(c);   // view: G rows interleaved with A rows
+        } else if (use_fused) {
+            CUDA_TRY(c, cudaMemsetAsync(c->d_G2, 0, bytes, c->stream), "model init");
         } else {
             cudaError_t e = cudaMalloc(&c->d_G, bytes);
             if (e != cudaSuccess) {
@@ -695,7 +710,7 @@ gcp_status gcp_grad_get(gcp_ctx* c, int k, double* out) {
     if (k < 0 || k >= c->d) return set_error(GCP_E_RANGE, "gcp_grad_get: mode out of range");
     if (!out) return set_error(GCP_E_ARG, "gcp_grad_get: NULL");
     ST_TRY(check_err(c, "gcp_grad_get"));
-    return read_rows(c, c->d_G, k, out, "grad_get");
+    return read_rows(c, cur_G(c), k, out, "grad_get");
 }
 
 gcp_status gcp_sample(gcp_ctx* c, gcp_strategy strategy, int64_t s_nz, int64_t s_z, uint64_t seed) {
@@ -803,6 +818,12 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
         return set_error(GCP_E_ARG, "gcp_adam_step: need 0 <= beta < 1, eps > 0, rate >= 0");
     const double lower = std::isnan(p->lower) ? loss_lower(c->last_loss) : p->lower;
     c->t += 1;
+    if (c->fused) {   // sync P > 1: reduce-scatter + Adam + all-gather in one NVLink kernel
+        ST_TRY(fused_exchange(c, p, lower));
+        c->it += 1;
+        c->have_grad = false;
+        return GCP_OK;
+    }
     Segment seg;
     seg.n = 0;
     const bool sharded = c->P > 1 && c->mode == GCP_DIST_SYNC;

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 #include <stdint.h>
 
 #include <string>
@@ -88,6 +89,12 @@ struct gcp_ctx {
     ncclComm_t slice[gcp::kMaxModes] = {nullptr};
     int slice_size[gcp::kMaxModes] = {0}, slice_rank[gcp::kMaxModes] = {0};
     bool ar_mode[gcp::kMaxModes] = {false};   // sync exchange of mode k: all-reduce (else RS/AG)
+    // fused NVLink exchange (fused.cu): symmetric windows + device communicator
+    bool fused = false, devcomm_ready = false;
+    ncclDevComm devcomm{};
+    ncclWindow_t winA = nullptr, winG[2] = {nullptr, nullptr};
+    void* d_G2 = nullptr;                         // second G buffer (iteration parity)
+    int fmem[gcp::kMaxModes][8] = {{0}}, fnmem[gcp::kMaxModes] = {0};
     int64_t tau = 0;
     gcp_adam_params server{};
     bool server_set = false;
@@ -184,5 +191,11 @@ gcp_status dist_sync_exchange_post(gcp_ctx* c);    // all-gather A
 gcp_status dist_async_sync(gcp_ctx* c);            // Alg. 3 averaging / Alg. 4 server step
 gcp_status dist_allreduce_scalar(gcp_ctx* c, double* dev_scalar);
 gcp_status dist_allreduce_i64_host(gcp_ctx* c, int64_t* v, int n);
+
+// fused.cu
+bool fused_possible(gcp_ctx* c);
+gcp_status fused_alloc(gcp_ctx* c, size_t bytes);   // A, G, G2 as symmetric windows (collective)
+void fused_free(gcp_ctx* c);
+gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower);
 
 }  // namespace gcp
