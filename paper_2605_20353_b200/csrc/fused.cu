@@ -67,11 +67,18 @@ __global__ void __launch_bounds__(256) k_fused_exchange(ncclDevComm comm, ncclWi
         const int64_t e = fa.off[k] + (fa.shard_start[k] + lv / vpr) * fa.R_pad + (lv % vpr) * VE;
         const size_t ob = (size_t)e * sizeof(T);
         // reduce-scatter: this shard vector of G^(k) summed over the slice group
-        V g = *reinterpret_cast<const V*>(ncclGetLsaPointer(winG, ob, fa.mem[k][0]));
+        // (all member loads issued before the adds: up to 8 NVLink loads in flight)
+        const int nm = fa.nmem[k];
+        V h[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+            if (m < nm) h[m] = *reinterpret_cast<const V*>(ncclGetLsaPointer(winG, ob, fa.mem[k][m]));
+        V g = h[0];
         T* gp = reinterpret_cast<T*>(&g);
-        for (int m = 1; m < fa.nmem[k]; ++m) {
-            const V h = *reinterpret_cast<const V*>(ncclGetLsaPointer(winG, ob, fa.mem[k][m]));
-            const T* hp = reinterpret_cast<const T*>(&h);
+#pragma unroll
+        for (int m = 1; m < 8; ++m) {
+            if (m >= nm) break;
+            const T* hp = reinterpret_cast<const T*>(&h[m]);
 #pragma unroll
             for (int q = 0; q < VE; ++q) gp[q] += hp[q];
         }
