@@ -253,7 +253,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--mode", default="sync", choices=["sync", "async", "fedadam"])
+    ap.add_argument("--mode", default="sync", choices=["sync", "twosided", "async", "fedadam"])
     ap.add_argument("--tau", type=int, default=10)
     ap.add_argument("--cpu-sample", type=int, default=100_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -299,7 +299,7 @@ def main():
     ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
     fp = ctx.fit_params(epochs=10 ** 6, iters_per_epoch=ITERS, max_fails=10 ** 6, s_nz=w["s"], s_z=w["s"],
                         f_nz=w["f"], f_z=w["f"], loss=w["loss"], seed=gcp_synth.SEEDS[name]["sample"], fseed=2,
-                        rate=1e-3, tau=args.tau if args.mode != "sync" else 0, meta_rate=1e-3)
+                        rate=1e-3, tau=args.tau if args.mode in ("async", "fedadam") else 0, meta_rate=1e-3)
     ctx.fit_begin(fp)
     log("warm-up")
     for _ in range(args.warmup):

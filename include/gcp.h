@@ -76,7 +76,13 @@ typedef enum { GCP_FP32 = 0, GCP_FP64 = 1 } gcp_precision;
 
 /* Multi-GPU scheme (P:642-749 sync, Alg. 2; P:435-450 LocalSGD, Alg. 3;
  * P:790-824 FedAdam, Alg. 4). */
-typedef enum { GCP_DIST_SYNC = 0, GCP_DIST_ASYNC_AVG = 1, GCP_DIST_ASYNC_FEDADAM = 2 } gcp_dist_mode;
+typedef enum {
+    GCP_DIST_SYNC = 0,            /* "all-reduce" factor layout: block rows replicated per slice group */
+    GCP_DIST_ASYNC_AVG = 1,       /* LocalSGD averaging every tau iterations (Alg. 3) */
+    GCP_DIST_ASYNC_FEDADAM = 2,   /* FedAdam server step every tau iterations (Alg. 4) */
+    GCP_DIST_SYNC_TWO_SIDED = 3   /* "two-sided" layout: rows partitioned, per-iteration import/export;
+                                     gcp_model_get and gcp_loss_estimate are collective in this mode */
+} gcp_dist_mode;
 
 /* Alg. 1 hyper-parameters.  lower: NaN selects the loss default. */
 typedef struct { double rate, beta1, beta2, eps, lower; } gcp_adam_params;

@@ -349,6 +349,7 @@ void gcp_destroy(gcp_ctx* c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (int k = 0; k < kMaxModes; ++k)
         if (c->slice[k]) ncclCommDestroy(c->slice[k]);
+    twosided_free(c);
     if (c->devcomm_ready) ncclDevCommDestroy(c->world, &c->devcomm);
     if (c->world) ncclCommDestroy(c->world);
     delete c;
@@ -531,10 +532,12 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     int64_t off = 0;
     for (int k = 0; k < c->d; ++k) {
         const int64_t b = c->hi[k] - c->lo[k];
-        const int64_t g = (c->P > 1 && c->mode == GCP_DIST_SYNC) ? c->slice_size[k] : 1;
+        const bool sy = c->P > 1 && sync_family(c);
+        const int64_t g = sy ? c->slice_size[k] : 1;
         // sync P > 1: every rank uses the same padded layout (ceil block size,
-        // multiple of the slice size), so the A / G windows are symmetric
-        const int64_t cb = (c->P > 1 && c->mode == GCP_DIST_SYNC) ? (c->dims[k] + c->grid[k] - 1) / c->grid[k] : b;
+        // multiple of the slice size), so the A / G windows are symmetric and
+        // shards (owned rows) are whole rows of equal size
+        const int64_t cb = sy ? (c->dims[k] + c->grid[k] - 1) / c->grid[k] : b;
         c->rows[k] = (cb + g - 1) / g * g;
         c->off[k] = off;
         off += c->rows[k] * c->R_pad;
@@ -546,7 +549,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         const std::string pol = env ? env : "auto";
         for (int k = 0; k < kMaxModes; ++k) {
             const double mb = k < c->d ? (double)c->rows[k] * c->R_pad * tsz(c) / 1048576.0 : 0;
-            c->ar_mode[k] = pol == "ar" || (pol == "auto" && mb <= 16.0);
+            c->ar_mode[k] = !two_sided(c) && (pol == "ar" || (pol == "auto" && mb <= 16.0));
         }
     }
     {
@@ -701,6 +704,7 @@ gcp_status gcp_model_get(gcp_ctx* c, int k, double* rows_out) {
     if (!c->have_model) return set_error(GCP_E_STATE, "gcp_model_get: no model");
     if (k < 0 || k >= c->d) return set_error(GCP_E_RANGE, "gcp_model_get: mode out of range");
     if (!rows_out) return set_error(GCP_E_ARG, "gcp_model_get: NULL");
+    if (two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // all-gather the owned rows (collective)
     return read_rows(c, c->d_A, k, rows_out, "model_get");
 }
 
@@ -782,11 +786,13 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     if (!c->have_model || !c->bound) return set_error(GCP_E_STATE, "gcp_loss_grad: need model and gcp_sample");
     if (!valid_loss(loss)) return set_error(GCP_E_ARG, "gcp_loss_grad: bad loss");
     // async schemes: averaging / server step before this iteration's sampling (Alg. 3-4)
-    if (c->mode != GCP_DIST_SYNC && c->tau > 0 && ((int64_t)c->it + 1) % c->tau == 0 && !c->have_grad)
+    if (async_family(c) && c->tau > 0 && ((int64_t)c->it + 1) % c->tau == 0 && !c->have_grad)
         ST_TRY(dist_async_sync(c));
     c->last_loss = loss;
     const int stratified = c->strategy == GCP_STRATIFIED;
     const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
+    // two-sided layout (row f3): touch pass + import of the rows owned elsewhere
+    if (two_sided(c) && !c->have_grad) ST_TRY(twosided_import(c, s));
     const ModelArgs m = model_args(c);
     const int with_loss = sampled_loss_out != nullptr;
     cudaEvent_t ev;
@@ -826,8 +832,17 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     }
     Segment seg;
     seg.n = 0;
-    const bool sharded = c->P > 1 && c->mode == GCP_DIST_SYNC;
-    if (sharded) {
+    const bool sharded = c->P > 1 && sync_family(c);
+    if (two_sided(c)) {
+        // row f3: imported rows' G back to their owners; Adam on the owned rows only
+        ST_TRY(twosided_export(c));
+        for (int k = 0; k < c->d; ++k) {
+            const int64_t shard = c->rows[k] / c->slice_size[k];
+            seg.start[seg.n] = c->off[k] + (int64_t)c->slice_rank[k] * shard * c->R_pad;
+            seg.len[seg.n] = shard * c->R_pad;
+            seg.n++;
+        }
+    } else if (sharded) {
         ST_TRY(dist_sync_exchange_pre(c));
         for (int k = 0; k < c->d; ++k) {
             if (c->ar_mode[k] || c->slice_size[k] <= 1) {   // replicated rows, all-reduced G
@@ -853,7 +868,7 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     prof_end(c, PROF_ADAM, ev);
     if (sharded) {
         CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, (size_t)c->n_coef * tsz(c), c->stream), "adam G reset");
-        ST_TRY(dist_sync_exchange_post(c));
+        if (!two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // two-sided: rows stay partitioned
     }
     c->it += 1;
     c->have_grad = false;
@@ -870,6 +885,7 @@ gcp_status gcp_loss_estimate(gcp_ctx* c, gcp_loss loss, int64_t f_nz, int64_t f_
     int64_t p, q;
     local_counts(c, f_nz, f_z, &p, &q);
     double* dout = (double*)c->d_partials + c->partials_cap;
+    if (two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // f-samples read any block row: refresh them
     ST_TRY(run_loss_kernel(c, loss, p, q, seed, 0xFFFFFFFFu, KIND_F_NZ, KIND_F_Z, 1, 0, PROF_LOSS, 1, dout));
     if (c->P > 1) ST_TRY(dist_allreduce_scalar(c, dout));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_scalar, dout, 8, cudaMemcpyDeviceToHost, c->stream), "loss_estimate");
@@ -884,14 +900,14 @@ gcp_status gcp_fit_begin(gcp_ctx* c, const gcp_fit_params* p, double* initial_es
     if (!c->have_model) return set_error(GCP_E_STATE, "gcp_fit_begin: no model");
     if (p->epochs < 0 || p->iters_per_epoch < 1 || p->max_fails < 1 || !(p->decay >= 0) || !valid_loss(p->loss))
         return set_error(GCP_E_ARG, "gcp_fit_begin: bad epoch parameters");
-    if (c->mode != GCP_DIST_SYNC && p->tau < 1) return set_error(GCP_E_ARG, "gcp_fit_begin: async needs tau >= 1");
+    if (async_family(c) && p->tau < 1) return set_error(GCP_E_ARG, "gcp_fit_begin: async needs tau >= 1");
     ST_TRY(gcp_sample(c, p->strategy, p->s_nz, p->s_z, p->seed));
     c->fp = *p;
     c->rate = p->adam.rate;
     c->fails = 0;
     c->epoch = 0;
     c->last_loss = p->loss;
-    if (c->mode != GCP_DIST_SYNC) {
+    if (async_family(c)) {
         c->tau = p->tau;
         if (!c->server_set) {
             c->server = p->adam;

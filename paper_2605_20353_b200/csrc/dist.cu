@@ -206,7 +206,8 @@ gcp_status gcp_dist_init(gcp_ctx* c, int nranks, int rank, const void* id, const
     if (!c) return set_error(GCP_E_ARG, "null context");
     if (c->sticky != GCP_OK) return set_error(GCP_E_STATE, "sticky error");
     if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(GCP_E_ARG, "gcp_dist_init: rank / nranks");
-    if (mode != GCP_DIST_SYNC && mode != GCP_DIST_ASYNC_AVG && mode != GCP_DIST_ASYNC_FEDADAM)
+    if (mode != GCP_DIST_SYNC && mode != GCP_DIST_ASYNC_AVG && mode != GCP_DIST_ASYNC_FEDADAM &&
+        mode != GCP_DIST_SYNC_TWO_SIDED)
         return set_error(GCP_E_ARG, "gcp_dist_init: mode");
     if (c->have_tensor) return set_error(GCP_E_STATE, "gcp_dist_init: must precede gcp_tensor_create");
     if (grid) {

@@ -94,6 +94,7 @@ struct gcp_ctx {
     ncclDevComm devcomm{};
     ncclWindow_t winA = nullptr, winG[2] = {nullptr, nullptr};
     void* d_G2 = nullptr;                         // second G buffer (iteration parity)
+    void* twosided = nullptr;                     // row f3 scratch (twosided.cu)
     int fmem[gcp::kMaxModes][8] = {{0}}, fnmem[gcp::kMaxModes] = {0};
     int64_t tau = 0;
     gcp_adam_params server{};
@@ -156,6 +157,15 @@ struct gcp_ctx {
 
 namespace gcp {
 
+// Alg. 2 schemes (one model, per-iteration exchange) vs Alg. 3 / 4 (replicas)
+inline bool sync_family(const gcp_ctx* c) {
+    return c->mode == GCP_DIST_SYNC || c->mode == GCP_DIST_SYNC_TWO_SIDED;
+}
+inline bool async_family(const gcp_ctx* c) {
+    return c->mode == GCP_DIST_ASYNC_AVG || c->mode == GCP_DIST_ASYNC_FEDADAM;
+}
+inline bool two_sided(const gcp_ctx* c) { return c->P > 1 && c->mode == GCP_DIST_SYNC_TWO_SIDED; }
+
 // thread-local error message + status helpers (api.cu)
 gcp_status set_error(gcp_status st, const std::string& msg);
 gcp_status cuda_fail(gcp_ctx* c, cudaError_t e, const char* what);
@@ -191,6 +201,11 @@ gcp_status dist_sync_exchange_post(gcp_ctx* c);    // all-gather A
 gcp_status dist_async_sync(gcp_ctx* c);            // Alg. 3 averaging / Alg. 4 server step
 gcp_status dist_allreduce_scalar(gcp_ctx* c, double* dev_scalar);
 gcp_status dist_allreduce_i64_host(gcp_ctx* c, int64_t* v, int n);
+
+// twosided.cu (row f3)
+gcp_status twosided_import(gcp_ctx* c, const SampleArgs& sa);
+gcp_status twosided_export(gcp_ctx* c);
+void twosided_free(gcp_ctx* c);
 
 // fused.cu
 bool fused_possible(gcp_ctx* c);

@@ -23,7 +23,7 @@ STATUS = {0: "GCP_OK", 1: "GCP_E_ARG", 2: "GCP_E_RANGE", 3: "GCP_E_DUP", 4: "GCP
 LOSS = {"gaussian": 0, "poisson": 1, "bernoulli": 2}
 STRATEGY = {"stratified": 0, "semi": 1}
 PRECISION = {"fp32": 0, "fp64": 1}
-DIST_MODE = {"sync": 0, "async": 1, "fedadam": 2}
+DIST_MODE = {"sync": 0, "async": 1, "fedadam": 2, "twosided": 3}
 PROF = {"grad": 0, "adam": 1, "loss": 2, "comm": 3, "other": 4}
 
 # every symbol include/gcp.h declares (checked by tests/test_abi.py)

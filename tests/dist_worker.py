@@ -49,17 +49,19 @@ def main():
         assert np.array_equal(ctx.model_get(k), A0[k][mine.lo[k]:mine.hi[k]]), "init"
 
     tau = 2
-    run = oracle.MultiRank(blocks, grid, A0, loss, mode=mode, tau=tau, meta_rate=5e-3)
+    # the two-sided layout (row f3) computes Alg. 2 exactly like the all-reduce layout
+    omode = "sync" if mode == "twosided" else mode
+    run = oracle.MultiRank(blocks, grid, A0, loss, mode=omode, tau=tau, meta_rate=5e-3)
     p = q = 600
     seed, rate = 99, 1e-2
     ctx.sample("stratified", p, q, seed)
-    if mode != "sync":
+    if omode != "sync":
         ctx.dist_set_async(tau, g.adam_params(rate=5e-3))
     ap = g.adam_params(rate=rate)
     worst = 0.0
     for it in range(5):
         # gradient of this rank's block, before any exchange
-        if mode == "sync":
+        if omode == "sync":
             A_rank = run.model_for_rank(rank)
             pw, qw = oracle.local_counts(mine, p, q, ws, rank)
             Go, S, _ = oracle.sampled_grad(mine, A_rank, loss, seed, rank, it, pw, qw)
