@@ -125,7 +125,7 @@ void free_model(gcp_ctx* c) {
     void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C, &c->d_lambda, &c->d_Ack, &c->d_Bck, &c->d_Cck,
                      &c->d_U,  &c->d_Bs, &c->d_Cs};
     for (void** b : bufs) {
-        cudaFree(*b);
+        gfree(c, *b);
         *b = nullptr;
     }
     c->have_model = false;
@@ -188,9 +188,9 @@ ModelArgs model_args(const gcp_ctx* c) {
 
 gcp_status ensure_partials(gcp_ctx* c, int n) {
     if (n <= c->partials_cap) return GCP_OK;
-    cudaFree(c->d_partials);
+    gfree(c, c->d_partials);
     c->d_partials = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->d_partials, sizeof(double) * (n + 1)), "partials");
+    CUDA_TRY(c, gmalloc(c, &c->d_partials, sizeof(double) * (n + 1)), "partials");
     c->partials_cap = n;
     return GCP_OK;
 }
@@ -242,9 +242,9 @@ gcp_status checkpoint_save(gcp_ctx* c) {
     const size_t bytes = (size_t)c->n_coef * tsz(c);
     const size_t abytes = a_elems(c) * tsz(c);   // A (with interleaved G rows, which are zero here)
     if (!c->d_Ack) {
-        CUDA_TRY(c, cudaMalloc(&c->d_Ack, abytes), "checkpoint alloc");
-        CUDA_TRY(c, cudaMalloc(&c->d_Bck, bytes), "checkpoint alloc");
-        CUDA_TRY(c, cudaMalloc(&c->d_Cck, bytes), "checkpoint alloc");
+        CUDA_TRY(c, gmalloc(c, &c->d_Ack, abytes), "checkpoint alloc");
+        CUDA_TRY(c, gmalloc(c, &c->d_Bck, bytes), "checkpoint alloc");
+        CUDA_TRY(c, gmalloc(c, &c->d_Cck, bytes), "checkpoint alloc");
     }
     CUDA_TRY(c, cudaMemcpyAsync(c->d_Ack, c->d_A, abytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
     CUDA_TRY(c, cudaMemcpyAsync(c->d_Bck, c->d_B, bytes, cudaMemcpyDeviceToDevice, c->stream), "checkpoint");
@@ -272,9 +272,9 @@ gcp_status server_reset(gcp_ctx* c) {
     if (c->mode != GCP_DIST_ASYNC_FEDADAM) return GCP_OK;
     const size_t bytes = (size_t)c->n_coef * tsz(c);
     if (!c->d_U) {
-        CUDA_TRY(c, cudaMalloc(&c->d_U, bytes), "server alloc");
-        CUDA_TRY(c, cudaMalloc(&c->d_Bs, bytes), "server alloc");
-        CUDA_TRY(c, cudaMalloc(&c->d_Cs, bytes), "server alloc");
+        CUDA_TRY(c, gmalloc(c, &c->d_U, bytes), "server alloc");
+        CUDA_TRY(c, gmalloc(c, &c->d_Bs, bytes), "server alloc");
+        CUDA_TRY(c, gmalloc(c, &c->d_Cs, bytes), "server alloc");
     }
     CUDA_TRY(c, cudaMemcpyAsync(c->d_U, c->d_A, bytes, cudaMemcpyDeviceToDevice, c->stream), "server reset");
     CUDA_TRY(c, cudaMemsetAsync(c->d_Bs, 0, bytes, c->stream), "server reset");
@@ -301,26 +301,29 @@ gcp_status gcp_create(gcp_ctx** out, int cuda_device, void* cuda_stream, gcp_pre
     if (e != cudaSuccess || ndev == 0) return set_error(GCP_E_CUDA, "gcp_create: no CUDA device");
     if (cuda_device < 0 || cuda_device >= ndev) return set_error(GCP_E_ARG, "gcp_create: bad device");
     DevGuard g(cuda_device);
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess)
-        return set_error(GCP_E_CUDA, "gcp_create: cudaGetDeviceProperties failed");
-    if (prop.major != 10) return set_error(GCP_E_CUDA, "gcp_create: libgcp is built for sm_100a (B200) only");
-    // Random 16-32 B record / bucket reads: ask L2 not to widen DRAM fetches
-    // (device-wide hint; GCP_L2_FETCH overrides, 0 leaves the driver default).
+    int major = 0, sms = 0, l2 = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cuda_device) != cudaSuccess)
+        return set_error(GCP_E_CUDA, "gcp_create: cudaDeviceGetAttribute failed");
+    if (major != 10) return set_error(GCP_E_CUDA, "gcp_create: libgcp is built for sm_100a (B200) only");
     {
-        const char* env = getenv("GCP_L2_FETCH");
-        const long v = env ? strtol(env, nullptr, 10) : 32;
-        if (v > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)v);
+        // stream-ordered pool keeps freed memory mapped for the next job (gmalloc)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
     }
     gcp_ctx* c = new gcp_ctx();
     c->dev = cuda_device;
     c->stream = (cudaStream_t)cuda_stream;
     c->prec = prec;
     c->tsize = prec == GCP_FP32 ? 4 : 8;
-    c->sm_count = prop.multiProcessorCount;
-    c->l2_bytes = prop.l2CacheSize;
+    c->sm_count = sms;
+    c->l2_bytes = l2;
     if (cudaMallocHost(&c->h_scalar, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess ||
-        cudaMalloc(&c->d_err, 64) != cudaSuccess) {
+        gmalloc(c, &c->d_err, 64) != cudaSuccess) {
         gcp_destroy(c);
         return set_error(GCP_E_OOM, "gcp_create: allocation failed");
     }
@@ -335,11 +338,11 @@ void gcp_destroy(gcp_ctx* c) {
     DevGuard g(c->dev);
     cudaStreamSynchronize(c->stream);
     free_model(c);
-    cudaFree(c->d_rec);
-    cudaFree(c->d_hash);
-    cudaFree(c->d_keys);
-    cudaFree(c->d_partials);
-    cudaFree(c->d_err);
+    gfree(c, c->d_rec);
+    gfree(c, c->d_hash);
+    gfree(c, c->d_keys);
+    gfree(c, c->d_partials);
+    gfree(c, c->d_err);
     if (c->h_scalar) cudaFreeHost(c->h_scalar);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto& p : c->pending) {
@@ -507,8 +510,8 @@ gcp_status gcp_tensor_contains(gcp_ctx* c, int64_t n, const int64_t* coords, int
     if (n == 0) return GCP_OK;
     int64_t* dc = nullptr;
     int8_t* dout = nullptr;
-    CUDA_TRY(c, cudaMalloc(&dc, sizeof(int64_t) * n * c->d), "contains");
-    CUDA_TRY(c, cudaMalloc(&dout, n), "contains");
+    CUDA_TRY(c, gmalloc(c, &dc, sizeof(int64_t) * n * c->d), "contains");
+    CUDA_TRY(c, gmalloc(c, &dout, n), "contains");
     CUDA_TRY(c, cudaMemcpyAsync(dc, coords, sizeof(int64_t) * n * c->d, cudaMemcpyHostToDevice, c->stream), "contains");
     cudaEvent_t ev;
     prof_begin(c, PROF_OTHER, &ev);
@@ -516,8 +519,8 @@ gcp_status gcp_tensor_contains(gcp_ctx* c, int64_t n, const int64_t* coords, int
     prof_end(c, PROF_OTHER, ev);
     CUDA_TRY(c, cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, c->stream), "contains");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream), "contains");
-    cudaFree(dc);
-    cudaFree(dout);
+    gfree(c, dc);
+    gfree(c, dout);
     return GCP_OK;
 }
 
@@ -576,7 +579,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         void** bufs[] = {&c->d_A, &c->d_B, &c->d_C};
         for (void** b : bufs) {
             if (use_fused && b == &c->d_A) continue;
-            cudaError_t e = cudaMalloc(b, b == &c->d_A && c->ag_interleaved ? 2 * bytes : bytes);
+            cudaError_t e = gmalloc(c, b, b == &c->d_A && c->ag_interleaved ? 2 * bytes : bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 free_model(c);
@@ -588,7 +591,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         } else if (use_fused) {
             CUDA_TRY(c, cudaMemsetAsync(c->d_G2, 0, bytes, c->stream), "model init");
         } else {
-            cudaError_t e = cudaMalloc(&c->d_G, bytes);
+            cudaError_t e = gmalloc(c, &c->d_G, bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 free_model(c);
@@ -596,7 +599,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
             }
         }
     }
-    CUDA_TRY(c, cudaMalloc(&c->d_lambda, (size_t)c->R_pad * tsz(c)), "model lambda");
+    CUDA_TRY(c, gmalloc(c, &c->d_lambda, (size_t)c->R_pad * tsz(c)), "model lambda");
     CUDA_TRY(c, cudaMemsetAsync(c->ag_interleaved ? c->d_A : c->d_G, 0, c->ag_interleaved ? 2 * bytes : bytes,
                                 c->stream),
              "model init");
@@ -753,10 +756,10 @@ gcp_status gcp_sample_export(gcp_ctx* c, int stratum, int64_t first, int64_t cou
     const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
     int64_t *d_subs = nullptr, *d_j = nullptr, *d_lo = nullptr;
     int32_t* d_att = nullptr;
-    CUDA_TRY(c, cudaMalloc(&d_subs, sizeof(int64_t) * count * c->d), "export");
-    CUDA_TRY(c, cudaMalloc(&d_j, sizeof(int64_t) * count), "export");
-    CUDA_TRY(c, cudaMalloc(&d_att, sizeof(int32_t) * count), "export");
-    CUDA_TRY(c, cudaMalloc(&d_lo, sizeof(int64_t) * kMaxModes), "export");
+    CUDA_TRY(c, gmalloc(c, &d_subs, sizeof(int64_t) * count * c->d), "export");
+    CUDA_TRY(c, gmalloc(c, &d_j, sizeof(int64_t) * count), "export");
+    CUDA_TRY(c, gmalloc(c, &d_att, sizeof(int32_t) * count), "export");
+    CUDA_TRY(c, gmalloc(c, &d_lo, sizeof(int64_t) * kMaxModes), "export");
     CUDA_TRY(c, cudaMemcpyAsync(d_lo, c->lo, sizeof(int64_t) * kMaxModes, cudaMemcpyHostToDevice, c->stream), "export");
     cudaEvent_t ev;
     prof_begin(c, PROF_OTHER, &ev);
@@ -770,10 +773,10 @@ gcp_status gcp_sample_export(gcp_ctx* c, int stratum, int64_t first, int64_t cou
         CUDA_TRY(c, cudaMemcpyAsync(attempts_out, d_att, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream),
                  "export");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream), "export");
-    cudaFree(d_subs);
-    cudaFree(d_j);
-    cudaFree(d_att);
-    cudaFree(d_lo);
+    gfree(c, d_subs);
+    gfree(c, d_j);
+    gfree(c, d_att);
+    gfree(c, d_lo);
     if (w_out) {
         const double w = stratum == 0 ? weight_nz(c, c->p_w) : weight_z(c, c->q_w);
         for (int64_t i = 0; i < count; ++i) w_out[i] = w;

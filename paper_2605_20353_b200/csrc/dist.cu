@@ -172,17 +172,17 @@ gcp_status dist_allreduce_scalar(gcp_ctx* c, double* dev_scalar) {
 
 gcp_status dist_allreduce_i64_host(gcp_ctx* c, int64_t* v, int n) {
     int64_t* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, sizeof(int64_t) * n);
+    cudaError_t e = gmalloc(c, &d, sizeof(int64_t) * n);
     if (e != cudaSuccess) return cuda_fail(c, e, "allreduce scratch");
     cudaMemcpyAsync(d, v, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream);
     ncclResult_t r = ncclAllReduce(d, d, n, ncclInt64, ncclSum, c->world, c->stream);
     if (r != ncclSuccess) {
-        cudaFree(d);
+        gfree(c, d);
         return nccl_fail(c, r, "ncclAllReduce(int64)");
     }
     cudaMemcpyAsync(v, d, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream);
     e = cudaStreamSynchronize(c->stream);
-    cudaFree(d);
+    gfree(c, d);
     if (e != cudaSuccess) return cuda_fail(c, e, "allreduce i64");
     return GCP_OK;
 }

@@ -214,3 +214,15 @@ void fused_free(gcp_ctx* c);
 gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower);
 
 }  // namespace gcp
+
+namespace gcp {
+// Device allocations come from the device's stream-ordered memory pool (its
+// release threshold is raised at gcp_create), so the multi-GB ingest scratch
+// and model buffers of repeated jobs reuse mapped memory instead of paying
+// cudaMalloc / cudaFree page mapping every time.
+template <typename P>
+inline cudaError_t gmalloc(gcp_ctx* c, P** p, size_t bytes) {
+    return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, c->stream);
+}
+inline cudaError_t gfree(gcp_ctx* c, void* p) { return p ? cudaFreeAsync(p, c->stream) : cudaSuccess; }
+}  // namespace gcp

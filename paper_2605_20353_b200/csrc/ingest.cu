@@ -227,17 +227,17 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
     uint64_t* new_hash = nullptr;
     uint64_t* new_keys = nullptr;
 
-    CK(cudaMalloc(&d_flags, sizeof(unsigned)));
+    CK(gmalloc(c, &d_flags, sizeof(unsigned)));
     CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
     if (nnz > 0) {
         // 1) stream the host COO through the staging buffer, converting on the fly
-        CK(cudaMalloc(&coords, (size_t)nnz * d * 4));
-        CK(cudaMalloc(&valt, (size_t)nnz * sizeof(T)));
-        CK(cudaMalloc(&k0, (size_t)nnz * 8));
-        if (k128) CK(cudaMalloc(&h0, (size_t)nnz * 8));
-        CK(cudaMalloc(&p0, (size_t)nnz * sizeof(PermT)));
-        CK(cudaMalloc(&d_sc, (size_t)chunk * d * 8));
-        CK(cudaMalloc(&d_vc, (size_t)chunk * 8));
+        CK(gmalloc(c, &coords, (size_t)nnz * d * 4));
+        CK(gmalloc(c, &valt, (size_t)nnz * sizeof(T)));
+        CK(gmalloc(c, &k0, (size_t)nnz * 8));
+        if (k128) CK(gmalloc(c, &h0, (size_t)nnz * 8));
+        CK(gmalloc(c, &p0, (size_t)nnz * sizeof(PermT)));
+        CK(gmalloc(c, &d_sc, (size_t)chunk * d * 8));
+        CK(gmalloc(c, &d_vc, (size_t)chunk * 8));
         for (int64_t b = 0; b < nnz; b += chunk) {
             const int64_t n = std::min(chunk, nnz - b);
             CK(cudaMemcpyAsync(d_sc, subs_h + b * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, st));
@@ -248,19 +248,19 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
         }
         CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        cudaFree(d_sc); d_sc = nullptr;
-        cudaFree(d_vc); d_vc = nullptr;
+        gfree(c, d_sc); d_sc = nullptr;
+        gfree(c, d_vc); d_vc = nullptr;
         if (flags & BAD_RANGE) { status = set_error(GCP_E_RANGE, "gcp_tensor_create: coordinate outside dims / block"); goto cleanup; }
         if (flags & BAD_VALUE) { status = set_error(GCP_E_ARG, "gcp_tensor_create: non-finite value"); goto cleanup; }
         // 2) LSD radix sort of (key, perm): low word, then stably the high word
-        CK(cudaMalloc(&k1, (size_t)nnz * 8));
-        CK(cudaMalloc(&p1, (size_t)nnz * sizeof(PermT)));
+        CK(gmalloc(c, &k1, (size_t)nnz * 8));
+        CK(gmalloc(c, &p1, (size_t)nnz * sizeof(PermT)));
         {
             cub::DoubleBuffer<uint64_t> keys(k0, k1);
             cub::DoubleBuffer<PermT> pm(p0, p1);
             const int lo_bits = k128 ? 64 : std::max(kbits, 1);
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, pm, nnz, 0, lo_bits, st));
-            CK(cudaMalloc(&tmp, tmp_bytes));
+            CK(gmalloc(c, &tmp, tmp_bytes));
             CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, pm, nnz, 0, lo_bits, st));
             if (k128) {
                 // high words in the current order, then a stable sort on them
@@ -272,9 +272,9 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
                 size_t tb2 = 0;
                 CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hk, pm, nnz, 0, kbits - 64, st));
                 if (tb2 > tmp_bytes) {
-                    cudaFree(tmp);
+                    gfree(c, tmp);
                     tmp = nullptr;
-                    CK(cudaMalloc(&tmp, tb2));
+                    CK(gmalloc(c, &tmp, tb2));
                     tmp_bytes = tb2;
                 }
                 CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, hk, pm, nnz, 0, kbits - 64, st));
@@ -288,32 +288,32 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
             CK(cudaGetLastError());
             c->launches++;
         }
-        cudaFree(tmp); tmp = nullptr;
-        cudaFree(k1); k1 = nullptr;
-        cudaFree(perm == p0 ? p1 : p0);
+        gfree(c, tmp); tmp = nullptr;
+        gfree(c, k1); k1 = nullptr;
+        gfree(c, perm == p0 ? p1 : p0);
         if (perm == p0) p1 = nullptr; else p0 = nullptr;
         // 3) duplicates, records
         k_dupcheck<<<nb, 256, 0, st>>>(nnz, skl, skh, d_flags);
         CK(cudaGetLastError());
         c->launches++;
-        CK(cudaMalloc(&new_rec, (size_t)nnz * rec_words * 4));
+        CK(gmalloc(c, &new_rec, (size_t)nnz * rec_words * 4));
         k_records<T, PermT><<<nb, 256, 0, st>>>(d, nnz, rec_words, perm, coords, valt, new_rec);
         CK(cudaGetLastError());
         c->launches++;
         CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (flags & BAD_DUP) { status = set_error(GCP_E_DUP, "gcp_tensor_create: duplicate coordinates"); goto cleanup; }
-        cudaFree(coords); coords = nullptr;
-        cudaFree(valt); valt = nullptr;
-        cudaFree(p0); p0 = nullptr;
-        cudaFree(p1); p1 = nullptr;
+        gfree(c, coords); coords = nullptr;
+        gfree(c, valt); valt = nullptr;
+        gfree(c, p0); p0 = nullptr;
+        gfree(c, p1); p1 = nullptr;
     } else {
-        CK(cudaMalloc(&new_rec, (size_t)rec_words * 4));
+        CK(gmalloc(c, &new_rec, (size_t)rec_words * 4));
     }
     // 4) zero-test structure
-    CK(cudaMalloc(&new_hash, (size_t)slots * 8 * kw));
+    CK(gmalloc(c, &new_hash, (size_t)slots * 8 * kw));
     CK(cudaMemsetAsync(new_hash, 0xFF, (size_t)slots * 8 * kw, st));
-    CK(cudaMalloc(&new_keys, (size_t)(sorted_member ? std::max<int64_t>(nnz, 1) : 1) * 8 * kw));
+    CK(gmalloc(c, &new_keys, (size_t)(sorted_member ? std::max<int64_t>(nnz, 1) : 1) * 8 * kw));
     if (nnz > 0) {
         if (sorted_member) k_store_keys<<<nb, 256, 0, st>>>(nnz, skl, skh, new_keys);
         else k_hash_insert<<<nb, 256, 0, st>>>(nnz, skl, skh, new_hash, slots - 1);
@@ -323,12 +323,12 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
     CK(cudaStreamSynchronize(st));
 
 cleanup:
-    cudaFree(d_flags); cudaFree(d_sc); cudaFree(d_vc); cudaFree(coords); cudaFree(valt);
-    cudaFree(k0); cudaFree(k1); cudaFree(h0); cudaFree(h1); cudaFree(p0); cudaFree(p1); cudaFree(tmp);
+    gfree(c, d_flags); gfree(c, d_sc); gfree(c, d_vc); gfree(c, coords); gfree(c, valt);
+    gfree(c, k0); gfree(c, k1); gfree(c, h0); gfree(c, h1); gfree(c, p0); gfree(c, p1); gfree(c, tmp);
     if (err != cudaSuccess || status != GCP_OK) {
-        cudaFree(new_rec);
-        cudaFree(new_hash);
-        cudaFree(new_keys);
+        gfree(c, new_rec);
+        gfree(c, new_hash);
+        gfree(c, new_keys);
         if (err == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             return set_error(GCP_E_OOM, "gcp_tensor_create: out of device memory");
@@ -337,9 +337,9 @@ cleanup:
         return status;
     }
     // commit
-    cudaFree(c->d_rec);
-    cudaFree(c->d_hash);
-    cudaFree(c->d_keys);
+    gfree(c, c->d_rec);
+    gfree(c, c->d_hash);
+    gfree(c, c->d_keys);
     c->d_rec = new_rec;
     c->d_hash = new_hash;
     c->d_keys = new_keys;

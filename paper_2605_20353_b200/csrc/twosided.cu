@@ -129,19 +129,19 @@ static int grid_for(const gcp_ctx* c, int64_t n) {
 template <typename P>
 static gcp_status grow(gcp_ctx* c, P** p, int64_t* cap, int64_t n, size_t elem) {
     if (n <= *cap) return GCP_OK;
-    cudaFree(*p);
+    gfree(c, *p);
     *p = nullptr;
     const int64_t want = std::max<int64_t>(n, *cap * 2);
-    TS_CUDA(c, cudaMalloc(p, (size_t)want * elem), "two-sided scratch");
+    TS_CUDA(c, gmalloc(c, p, (size_t)want * elem), "two-sided scratch");
     *cap = want;
     return GCP_OK;
 }
 static gcp_status grow_b(gcp_ctx* c, void** p, size_t* cap, size_t bytes) {
     if (bytes <= *cap) return GCP_OK;
-    cudaFree(*p);
+    gfree(c, *p);
     *p = nullptr;
     const size_t want = std::max(bytes, *cap * 2);
-    TS_CUDA(c, cudaMalloc(p, want), "two-sided buffer");
+    TS_CUDA(c, gmalloc(c, p, want), "two-sided buffer");
     *cap = want;
     return GCP_OK;
 }
@@ -150,17 +150,17 @@ void twosided_free(gcp_ctx* c) {
     TwoSidedState* s = static_cast<TwoSidedState*>(c->twosided);
     if (!s) return;
     for (int k = 0; k < kMaxModes; ++k) {
-        cudaFree(s->bitmap[k]);
-        cudaFree(s->need[k]);
-        cudaFree(s->req[k]);
+        gfree(c, s->bitmap[k]);
+        gfree(c, s->need[k]);
+        gfree(c, s->req[k]);
     }
-    cudaFree(s->flags);
-    cudaFree(s->d_counts);
+    gfree(c, s->flags);
+    gfree(c, s->d_counts);
     if (s->h_counts) cudaFreeHost(s->h_counts);
-    cudaFree(s->sbuf);
-    cudaFree(s->rbuf);
-    cudaFree(s->cub_tmp);
-    cudaFree(s->d_nsel);
+    gfree(c, s->sbuf);
+    gfree(c, s->rbuf);
+    gfree(c, s->cub_tmp);
+    gfree(c, s->d_nsel);
     delete s;
     c->twosided = nullptr;
 }
@@ -169,9 +169,9 @@ static gcp_status state(gcp_ctx* c, TwoSidedState** out) {
     if (!c->twosided) {
         TwoSidedState* s = new TwoSidedState();
         c->twosided = s;
-        TS_CUDA(c, cudaMalloc(&s->d_counts, sizeof(int64_t) * kMaxModes * (8 + 64)), "two-sided counts");
+        TS_CUDA(c, gmalloc(c, &s->d_counts, sizeof(int64_t) * kMaxModes * (8 + 64)), "two-sided counts");
         TS_CUDA(c, cudaMallocHost(&s->h_counts, sizeof(int64_t) * kMaxModes * (8 + 64)), "two-sided counts");
-        TS_CUDA(c, cudaMalloc(&s->d_nsel, sizeof(int64_t) * kMaxModes), "two-sided counts");
+        TS_CUDA(c, gmalloc(c, &s->d_nsel, sizeof(int64_t) * kMaxModes), "two-sided counts");
     }
     *out = static_cast<TwoSidedState*>(c->twosided);
     return GCP_OK;
