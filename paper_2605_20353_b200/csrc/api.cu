@@ -118,7 +118,15 @@ double u128_to_double(unsigned __int128 v) { return (double)v; }
 
 double loss_lower(int loss) { return loss == GCP_LOSS_POISSON ? 0.0 : -INFINITY; }
 
+// The captured epoch graph bakes in buffer pointers, sample counts and the
+// iteration schedule: any change to them drops it (rebuilt on the next epoch).
+void graph_drop(gcp_ctx* c) {
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+}
+
 void free_model(gcp_ctx* c) {
+    graph_drop(c);
     fused_free(c);                             // symmetric A / G windows (collective)
     if (c->ag_interleaved) c->d_G = nullptr;   // a view into d_A
     c->ag_interleaved = false;
@@ -167,6 +175,11 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     s.member_sorted = c->member == GCP_MEMBER_SORTED;
     s.keys = c->d_keys;
     s.err_slot = c->d_err;
+    s.it_dev = nullptr;
+    if (c->capturing) {   // epoch graph: this launch's iteration relative to the replay's first
+        s.it_dev = &c->d_step->it;
+        s.it = it - c->graph_it0;
+    }
     return s;
 }
 
@@ -343,6 +356,8 @@ void gcp_destroy(gcp_ctx* c) {
     gfree(c, c->d_keys);
     gfree(c, c->d_partials);
     gfree(c, c->d_err);
+    gfree(c, c->d_step);
+    if (c->h_step) cudaFreeHost(c->h_step);
     if (c->h_scalar) cudaFreeHost(c->h_scalar);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto& p : c->pending) {
@@ -366,6 +381,7 @@ gcp_status gcp_dist_set_async(gcp_ctx* c, int64_t tau, const gcp_adam_params* se
         c->server = *server;
         c->server_set = true;
     }
+    graph_drop(c);
     return GCP_OK;
 }
 
@@ -373,6 +389,7 @@ gcp_status gcp_set_membership(gcp_ctx* c, gcp_membership m) {
     ENTER(c);
     if (m != GCP_MEMBER_HASH && m != GCP_MEMBER_SORTED) return set_error(GCP_E_ARG, "gcp_set_membership: bad value");
     c->member = m;
+    graph_drop(c);
     return GCP_OK;
 }
 
@@ -740,6 +757,7 @@ gcp_status gcp_sample(gcp_ctx* c, gcp_strategy strategy, int64_t s_nz, int64_t s
     c->q_w = q_w;
     c->seed = seed;
     c->bound = true;
+    graph_drop(c);
     return GCP_OK;
 }
 
@@ -865,8 +883,9 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     }
     cudaEvent_t ev;
     prof_begin(c, PROF_ADAM, &ev);
-    CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower, c->t,
-                            sharded ? 0 : 1, c->ag_stride),
+    CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower,
+                            c->capturing ? c->t - c->graph_t0 : c->t, sharded ? 0 : 1, c->ag_stride,
+                            c->capturing ? c->d_step : nullptr),
              "gcp_adam_step");
     prof_end(c, PROF_ADAM, ev);
     if (sharded) {
@@ -927,6 +946,89 @@ gcp_status gcp_fit_begin(gcp_ctx* c, const gcp_fit_params* p, double* initial_es
     return GCP_OK;
 }
 
+// An epoch's iterations (K2 + Adam / exchange) are one CUDA graph:
+// captured once per schedule, replayed with the step state (t0, it0, rate)
+// uploaded to device memory; each captured launch adds its own offset, so the
+// replay needs no host work per iteration.  Not used on
+// the legacy stream (uncapturable), while profiling (per-kernel events), for
+// the two-sided layout (host-sized transfers) or FedAdam (host server clock).
+static bool graph_ok(const gcp_ctx* c) {
+    const char* env = getenv("GCP_GRAPHS");
+    if (env && atoi(env) == 0) return false;
+    return c->stream != nullptr && !c->prof_on && !two_sided(c) && c->mode != GCP_DIST_ASYNC_FEDADAM;
+}
+
+static gcp_status epoch_graph(gcp_ctx* c, gcp_loss loss, const gcp_adam_params& ap, int iters) {
+    if (!c->d_step) {
+        CUDA_TRY(c, gmalloc(c, &c->d_step, sizeof(DevStep)), "step state");
+        CUDA_TRY(c, cudaMallocHost(&c->h_step, sizeof(DevStep)), "step state");
+    }
+    const double lower = std::isnan(ap.lower) ? loss_lower(loss) : ap.lower;
+    const int64_t period = 2 * std::max<int64_t>(c->tau, 1);   // G parity and the async schedule
+    const double key[8] = {(double)iters, (double)((int64_t)c->it % period), ap.beta1, ap.beta2, ap.eps, lower,
+                           (double)loss, (double)c->fused};
+    const uint32_t it0 = c->it;
+    const int64_t t0 = c->t;
+    if (!c->graph_exec || memcmp(key, c->graph_key, sizeof(key)) != 0) {
+        graph_drop(c);
+        // a schedule seen once runs eagerly (a one-epoch job would pay the
+        // capture and instantiation for nothing); the second sighting captures
+        if (!c->graph_seen_valid || memcmp(key, c->graph_seen, sizeof(key)) != 0) {
+            memcpy(c->graph_seen, key, sizeof(key));
+            c->graph_seen_valid = true;
+            for (int i = 0; i < iters; ++i) {
+                ST_TRY(gcp_loss_grad(c, loss, nullptr));
+                ST_TRY(gcp_adam_step(c, &ap));
+            }
+            return GCP_OK;
+        }
+        const int64_t l0 = c->launches;
+        c->graph_it0 = it0;
+        c->graph_t0 = t0;
+        CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+        c->capturing = true;
+        gcp_status st = GCP_OK;
+        for (int i = 0; i < iters && st == GCP_OK; ++i) {
+            st = gcp_loss_grad(c, loss, nullptr);
+            if (st == GCP_OK) st = gcp_adam_step(c, &ap);
+        }
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        c->capturing = false;
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+        c->it = it0;
+        c->t = t0;
+        c->have_grad = false;
+        if (st != GCP_OK || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            if (st != GCP_OK) return st;
+            return cuda_fail(c, e, "graph capture");
+        }
+        const cudaError_t ei = cudaGraphInstantiate(&c->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) {
+            c->graph_exec = nullptr;
+            return cuda_fail(c, ei, "graph instantiate");
+        }
+        memcpy(c->graph_key, key, sizeof(key));
+    }
+    DevStep* h = c->h_step;
+    h->rate = ap.rate;
+    h->beta1 = ap.beta1;
+    h->beta2 = ap.beta2;
+    h->t = t0;
+    h->it = it0;
+    h->pad = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_step, h, sizeof(DevStep), cudaMemcpyHostToDevice, c->stream), "step state");
+    CUDA_TRY(c, cudaGraphLaunch(c->graph_exec, c->stream), "graph launch");
+    c->it = it0 + (uint32_t)iters;
+    c->t = t0 + iters;
+    c->launches += c->graph_launches;
+    c->have_grad = false;
+    return GCP_OK;
+}
+
 gcp_status gcp_fit_epoch(gcp_ctx* c, double* est_out, int* accepted_out, int* done_out) {
     ENTER(c);
     if (!c->fit_active) return set_error(GCP_E_STATE, "gcp_fit_epoch: call gcp_fit_begin first");
@@ -937,10 +1039,13 @@ gcp_status gcp_fit_epoch(gcp_ctx* c, double* est_out, int* accepted_out, int* do
     }
     gcp_adam_params ap = p.adam;
     ap.rate = c->rate;
-    for (int i = 0; i < p.iters_per_epoch; ++i) {
-        ST_TRY(gcp_loss_grad(c, p.loss, nullptr));
-        ST_TRY(gcp_adam_step(c, &ap));
-    }
+    if (graph_ok(c))
+        ST_TRY(epoch_graph(c, p.loss, ap, p.iters_per_epoch));
+    else
+        for (int i = 0; i < p.iters_per_epoch; ++i) {
+            ST_TRY(gcp_loss_grad(c, p.loss, nullptr));
+            ST_TRY(gcp_adam_step(c, &ap));
+        }
     double est;
     ST_TRY(gcp_loss_estimate(c, p.loss, p.f_nz, p.f_z, p.fseed, &est));
     int accepted = est < c->best;

@@ -34,6 +34,10 @@ __device__ __forceinline__ U64x2 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
 // floor(W * n / 2^64): an exact integer map of a uniform 64-bit word onto [0, n).
 __device__ __forceinline__ uint64_t range_map(uint64_t W, uint64_t n) { return __umul64hi(W, n); }
 
+// Philox iteration word: inside a replayed epoch graph the replay's first
+// iteration (device memory) plus this launch's offset, else the launch argument.
+__device__ __forceinline__ uint32_t iter_word(const SampleArgs& a) { return a.it_dev ? *a.it_dev + a.it : a.it; }
+
 // ---- hashing ------------------------------------------------------------------
 __device__ __host__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64 finaliser
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -135,7 +139,7 @@ __device__ __forceinline__ void zero_candidate(const SampleArgs& a, uint32_t zs,
     const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
 #pragma unroll
     for (int g = 0; g < (D + 1) / 2; ++g) {
-        const U64x2 w = philox(zs, a.rank, (a.kind_z << 28) | (att << 4) | (uint32_t)g, a.it, k0, k1);
+        const U64x2 w = philox(zs, a.rank, (a.kind_z << 28) | (att << 4) | (uint32_t)g, iter_word(a), k0, k1);
         c[2 * g] = (uint32_t)range_map(w.w0, a.bdim[2 * g]);
         if (2 * g + 1 < D) c[2 * g + 1] = (uint32_t)range_map(w.w1, a.bdim[2 * g + 1]);
     }
@@ -170,7 +174,7 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
     constexpr int VW = (int)(sizeof(T) / 4);
     if (s < a.p) {
         // nonzero slot: j uniform over [0, N) with replacement
-        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, a.it, k0, k1);
+        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, iter_word(a), k0, k1);
         const uint64_t j = range_map(w.w0, (uint64_t)a.N);
         const uint4* r = reinterpret_cast<const uint4*>(a.rec + j * a.rec_words);
         P.w0 = __ldg(r);
@@ -252,7 +256,7 @@ __device__ __forceinline__ Sample<T, D> resolve_sample(const SampleArgs& a, cons
         for (int k = 0; k < D; ++k) o.c[k] = w8[(VW + k) & 7];
         uint64_t j = P.j;
         if ((uint64_t)a.N > 0xFFFFFFFFull) {
-            const U64x2 w = philox(P.slot, a.rank, a.kind_nz << 28, a.it, (uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+            const U64x2 w = philox(P.slot, a.rank, a.kind_nz << 28, iter_word(a), (uint32_t)a.seed, (uint32_t)(a.seed >> 32));
             j = range_map(w.w0, (uint64_t)a.N);
         }
         o.j = (int64_t)j;

@@ -44,9 +44,16 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_fused_exchange(ncclDevComm comm, ncclWindow_t winA, ncclWindow_t winG,
                                                         T* __restrict__ gzero, T* __restrict__ B,
                                                         T* __restrict__ C, const FusedArgs fa, T rate, T b1, T b2,
-                                                        T eps, T bc1, T bc2, T lower) {
+                                                        T eps, T bc1, T bc2, T lower, const DevStep* step,
+                                                        long long t_off) {
     using V = typename FVec<T>::type;
     constexpr int VE = FVec<T>::n;
+    if (step) {   // graph replay: t = t0 + offset, bias corrections in fp64 from it
+        const double t = (double)(step->t + t_off);
+        rate = (T)step->rate;
+        bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
+        bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
+    }
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamLsa(comm), comm.lsaBarrier, blockIdx.x);
     // every rank's K2 of this iteration is complete (stream order before arrive)
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
@@ -209,11 +216,13 @@ gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower) {
     if (c->prec == GCP_FP32)
         k_fused_exchange<float><<<kFusedCTAs, 256, 0, c->stream>>>(
             c->devcomm, c->winA, c->winG[cur], (float*)gnext, (float*)c->d_B, (float*)c->d_C, fa, (float)p->rate,
-            (float)p->beta1, (float)p->beta2, (float)p->eps, (float)bc1, (float)bc2, (float)lower);
+            (float)p->beta1, (float)p->beta2, (float)p->eps, (float)bc1, (float)bc2, (float)lower,
+            c->capturing ? c->d_step : nullptr, (long long)(c->t - c->graph_t0));
     else
         k_fused_exchange<double><<<kFusedCTAs, 256, 0, c->stream>>>(
             c->devcomm, c->winA, c->winG[cur], (double*)gnext, (double*)c->d_B, (double*)c->d_C, fa, p->rate,
-            p->beta1, p->beta2, p->eps, bc1, bc2, lower);
+            p->beta1, p->beta2, p->eps, bc1, bc2, lower, c->capturing ? c->d_step : nullptr,
+            (long long)(c->t - c->graph_t0));
     prof_end(c, PROF_COMM, ev);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "fused exchange");

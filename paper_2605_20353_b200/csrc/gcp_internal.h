@@ -51,6 +51,17 @@ struct SampleArgs {
     int member_sorted;        // 1: binary search of `keys` instead of the hash set (row f4)
     const uint64_t* keys;     // sorted block keys (u64, or (lo,hi) pairs for u128)
     unsigned long long* err_slot;  // min zero slot that hit the rejection cap (ULLONG_MAX = none)
+    const uint32_t* it_dev;   // non-null inside a captured epoch graph: it = *it_dev + it (offset)
+};
+
+// Epoch-graph replay state: the values of rate, t and it at the start of the
+// replay, uploaded once per replay.  Each captured kernel carries its own
+// iteration offset as a launch argument (t = t0 + off, it = it0 + off), so no
+// kernel has to advance a device counter.
+struct DevStep {
+    double rate, beta1, beta2;
+    long long t;
+    uint32_t it, pad;
 };
 
 struct ModelArgs {
@@ -140,6 +151,17 @@ struct gcp_ctx {
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;  // pinned
     int grad_blocks = 0;                // persistent grid of the sample kernels
+    // ---- epoch graph (gcp_fit_epoch): captured once per (fit, phase) key, replayed
+    gcp::DevStep* d_step = nullptr;     // device step state read by K2 / Adam during replay
+    gcp::DevStep* h_step = nullptr;     // pinned staging for the per-replay upload
+    bool capturing = false;
+    cudaGraphExec_t graph_exec = nullptr;
+    double graph_key[8] = {0};
+    double graph_seen[8] = {0};         // key of the last eager epoch: capture on the second sighting
+    bool graph_seen_valid = false;
+    int64_t graph_launches = 0;         // library launches recorded in the graph
+    uint32_t graph_it0 = 0;             // it / t at the start of the capture: launch offsets are relative
+    int64_t graph_t0 = 0;
     // ---- fit state
     bool fit_active = false;
     gcp_fit_params fp{};
@@ -184,7 +206,8 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C,
                         double rate, double beta1, double beta2, double eps, double lower,
-                        int64_t t, int zero_g, int row_stride = 0);   // row_stride 0: contiguous A/G
+                        int64_t t, int zero_g, int row_stride = 0,    // row_stride 0: contiguous A/G
+                        const DevStep* step = nullptr);               // step: t = step->t + t (offset), rate
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
 cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);

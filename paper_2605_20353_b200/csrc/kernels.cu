@@ -15,9 +15,9 @@ cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int6
 cudaError_t export_f64(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
                        int32_t*);
 cudaError_t adam_f32(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int);
+                     double, int64_t, int, int, int, const DevStep*);
 cudaError_t adam_f64(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int);
+                     double, int64_t, int, int, int, const DevStep*);
 cudaError_t init_f32(gcp_ctx*, const InitArgs&, void*);
 cudaError_t init_f64(gcp_ctx*, const InitArgs&, void*);
 
@@ -43,10 +43,11 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
 
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                         double beta1, double beta2, double eps, double lower, int64_t t, int zero_g,
-                        int row_stride) {
+                        int row_stride, const DevStep* step) {
     const int rs = row_stride > 0 ? row_stride : c->R_pad;
-    return c->prec == GCP_FP32 ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs)
-                               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs);
+    return c->prec == GCP_FP32
+               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step)
+               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step);
 }
 
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {

@@ -228,9 +228,16 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
                                               T* __restrict__ G, T* __restrict__ B, T* __restrict__ C,
                                               T rate, T b1, T b2, T eps, T bc1, T bc2, T lower,
-                                              int zero_g, int R_pad, int row_stride) {
+                                              int zero_g, int R_pad, int row_stride, const DevStep* step,
+                                              long long t_off) {
     using V = typename Vec16<T>::type;
     constexpr int VE = Vec16<T>::n;
+    if (step) {   // graph replay: t = t0 + offset, bias corrections in fp64 from it
+        const double t = (double)(step->t + t_off);
+        rate = (T)step->rate;
+        bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
+        bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec_total;
          i += (int64_t)gridDim.x * blockDim.x) {
         // map the virtual vector index onto its segment

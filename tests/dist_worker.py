@@ -83,6 +83,28 @@ def main():
     oe, sc = run.estimate(5, 1500, 1500)
     assert abs(est - oe) <= 1e-10 * sc, (est, oe)
     ctx.close()
+
+    # the epoch loop (R20) on a side stream: the iterations of an epoch replay
+    # as one CUDA graph (sync / twosided-off / LocalSGD) -- against oracle.fit
+    stream = torch.cuda.Stream(local)
+    uid = [g.gcp_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ctx = g.Context(local, stream.cuda_stream, "fp64")
+    ctx.dist_init(ws, rank, uid[0], None, mode)
+    ctx.tensor_create(dims, bs, bv)
+    ctx.model_init(R, 77)
+    kw = dict(epochs=3, max_fails=3, decay=0.1, s_nz=p, s_z=q, f_nz=1500, f_z=1500, seed=seed, fseed=5,
+              rate=rate)
+    fp = ctx.fit_params(iters_per_epoch=6, loss=loss, tau=tau if omode != "sync" else 0, meta_rate=5e-3, **kw)
+    best, rows = ctx.fit(fp)
+    Af, hist, obest = oracle.fit(blocks, grid, A0, loss, iters=6, mode=omode, tau=tau, meta_rate=5e-3, **kw)
+    assert len(rows) == len(hist), (rows, hist)
+    for r, h in zip(rows, hist):
+        assert abs(r[2] - h[0]) <= 1e-9 * abs(h[0]), (r, h)
+    for k in range(3):
+        want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
+        assert np.allclose(ctx.model_get(k), want, rtol=1e-8, atol=1e-10), f"fit model k={k}"
+    ctx.close()
     dist.barrier()
     if rank == 0:
         print(f"DIST-OK mode={mode} P={ws} grid={grid} worst_model_err={worst:.2e}", flush=True)

@@ -282,6 +282,38 @@ def test_sorted_membership_same_draws(gcp, orc, shape):
     _grad_check(G, Go, S, 1e-4, "sorted membership")
 
 
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_fit_matches_oracle(gcp, orc, graphs, monkeypatch):
+    """The epoch loop (annealing, R20) against oracle.fit, fp64, on a side
+    stream: with GCP_GRAPHS=1 each epoch's iterations replay as one CUDA graph
+    with the step state on the device; with 0 they launch one by one."""
+    import torch
+    monkeypatch.setenv("GCP_GRAPHS", graphs)
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    stream = torch.cuda.Stream(0)
+    c = gcp.Context(0, stream.cuda_stream, "fp64")
+    c.tensor_create(dims, subs, vals)
+    c.model_init(4, 2001)
+    A0 = _model(c, 3)
+    kw = dict(epochs=6, max_fails=3, decay=0.1, s_nz=300, s_z=300, f_nz=1500, f_z=1500, seed=7, fseed=2,
+              rate=0.3)
+    p = c.fit_params(iters_per_epoch=10, loss="poisson", **kw)
+    best, rows = c.fit(p)
+    blocks, grid = orc.split_blocks(dims, subs, vals, 1)
+    Af, hist, obest = orc.fit(blocks, grid, A0, "poisson", iters=10, **kw)
+    assert len(rows) == len(hist)
+    for (_, _, est, rate, _), (oest, orate, _) in zip(rows, hist):
+        assert est == pytest.approx(oest, rel=1e-9)
+    assert [r[3] for r in rows] == pytest.approx([h[1] * (1.0 if h[2] else kw["decay"]) for h in hist])
+    assert best == pytest.approx(obest, rel=1e-9)
+    for k in range(3):
+        assert np.allclose(c.model_get(k), Af[k], rtol=1e-8, atol=1e-10)
+    cnt = c.counters()
+    assert cnt["it"] == 10 * len(rows)   # t rolls back with a rejected epoch, it does not
+    assert cnt["t"] == 10 * sum(h[2] for h in hist)
+
+
 def test_fit_runs_and_decreases(gcp, orc):
     dims = (20, 30, 40)
     subs, vals = _tensor("poisson")
