@@ -155,6 +155,15 @@ def allmax(ws, x):
     return float(t.item())
 
 
+def allgather_obj(ws, o):
+    if ws == 1:
+        return [o]
+    import torch.distributed as dist
+    out = [None] * ws
+    dist.all_gather_object(out, o)
+    return out
+
+
 def bcast_bytes(ws, rank, b):
     if ws == 1:
         return b
@@ -297,6 +306,7 @@ def main():
     ctx.tensor_create_ptr(w["dims"], nnz_local, subs_h.data_ptr(), vals_h.data_ptr())
     ingest_s = time.time() - t0
     ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
+    features = ctx.dist_features()
     fp = ctx.fit_params(epochs=10 ** 6, iters_per_epoch=ITERS, max_fails=10 ** 6, s_nz=w["s"], s_z=w["s"],
                         f_nz=w["f"], f_z=w["f"], loss=w["loss"], seed=gcp_synth.SEEDS[name]["sample"], fseed=2,
                         rate=1e-3, tau=args.tau if args.mode in ("async", "fedadam") else 0, meta_rate=1e-3)
@@ -329,6 +339,7 @@ def main():
         ctx.fit_epoch()
     prof = {k: ctx.profile_get(k) for k in g.gcp.PROF}
     ctx.profile_enable(False)
+    prof_ranks = allgather_obj(ws, {k: v[0] / prof_epochs for k, v in prof.items()})
     ms_step = ms / args.steps
     eps = 1000.0 / ms_step
     samples_per_s = eps * ITERS * (2 * w["s"])
@@ -372,6 +383,8 @@ def main():
             "config": {"workload": f"{name}: {w['desc']}", "dims": list(w["dims"]), "nnz": int(w["nnz"]),
                        "R": w["R"], "loss": w["loss"], "p": w["s"], "q": w["s"], "f_nz": w["f"], "f_z": w["f"],
                        "iters_per_epoch": ITERS, "grid": list(grid), "dist_mode": args.mode,
+                       "exchange": ("none" if ws == 1 else "fused-nvlink-multimem" if features["multimem"]
+                                    else "fused-nvlink" if features["fused"] else "nccl"),
                        "parallelism": f"grid{'x'.join(map(str, grid))}-{args.mode}" if ws > 1 else "single-gpu",
                        "l2": ("inputs larger than L2 (COO records + hash set >> 126 MB); factors "
                               + ("stay L2-resident" if sum(w["dims"]) * w["R"] * 4 < 32e6
@@ -382,6 +395,7 @@ def main():
             "gpu_launches": int(launches),
             "library_launches_total": int(c1["launches"] - c0["launches"]),
             "phase_ms_per_step": {k: v[0] / prof_epochs for k, v in prof.items()},
+            "phase_ms_per_step_ranks": prof_ranks if ws > 1 else None,
             "phase_source": f"library CUDA events over {prof_epochs} extra untimed epochs (rank 0)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "k_sample (K2 fused sampling-MTTKRP)",

@@ -268,6 +268,18 @@ gcp_status gcp_fit(gcp_ctx* ctx, const gcp_fit_params* p, gcp_trace_fn trace, vo
  * by this library since creation (all nullable).  Does not block. */
 gcp_status gcp_counters(gcp_ctx* ctx, uint32_t* it, int64_t* t, int64_t* launches);
 
+/* Which sync exchange the model runs (a6-a8), for
+ * benchmarks and tests; both nullable, set after gcp_model_init:
+ *   *fused_out    = 1 when reduce-scatter + Adam + all-gather is the single
+ *                   NVLink kernel over symmetric windows (else NCCL calls);
+ *   *multimem_out = 1 when that kernel sums and broadcasts the modes whose
+ *                   slice group spans all ranks through NVLS multicast
+ *                   (reduction inside the NVSwitch; fp32 only; environment
+ *                   GCP_MULTIMEM=1 forces it, 0 disables it, default from
+ *                   8 ranks up).
+ * Does not block. */
+gcp_status gcp_dist_features(gcp_ctx* ctx, int* fused_out, int* multimem_out);
+
 /* Enable (1) / disable (0) CUDA-event timing of every library kernel launch on
  * the context stream (the events bracket each launch; adds no sync). */
 gcp_status gcp_profile_enable(gcp_ctx* ctx, int on);

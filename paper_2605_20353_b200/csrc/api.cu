@@ -1083,6 +1083,15 @@ gcp_status gcp_fit(gcp_ctx* c, const gcp_fit_params* p, gcp_trace_fn trace, void
     return GCP_OK;
 }
 
+gcp_status gcp_dist_features(gcp_ctx* c, int* fused_out, int* multimem_out) {
+    ENTER(c);
+    if (fused_out) *fused_out = c->fused ? 1 : 0;
+    int mm = 0;
+    for (int k = 0; k < c->d; ++k) mm |= fused_use_multimem(c) && c->fnmem[k] == c->P;
+    if (multimem_out) *multimem_out = mm;
+    return GCP_OK;
+}
+
 gcp_status gcp_counters(gcp_ctx* c, uint32_t* it, int64_t* t, int64_t* launches) {
     if (!c) return set_error(GCP_E_ARG, "null context");
     if (it) *it = c->it;

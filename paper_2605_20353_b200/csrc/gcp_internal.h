@@ -102,6 +102,11 @@ struct gcp_ctx {
     bool ar_mode[gcp::kMaxModes] = {false};   // sync exchange of mode k: all-reduce (else RS/AG)
     // fused NVLink exchange (fused.cu): symmetric windows + device communicator
     bool fused = false, devcomm_ready = false;
+    bool multimem = false;                        // NVLS multicast usable on the LSA team
+    int fused_ctas = 0;                           // grid of the fused exchange (one LSA barrier each)
+    void* ftrace = nullptr;                       // GCP_FUSED_TRACE diagnostics
+    double ftrace_acc[16] = {0};
+    int64_t ftrace_n = 0;
     ncclDevComm devcomm{};
     ncclWindow_t winA = nullptr, winG[2] = {nullptr, nullptr};
     void* d_G2 = nullptr;                         // second G buffer (iteration parity)
@@ -232,6 +237,7 @@ void twosided_free(gcp_ctx* c);
 
 // fused.cu
 bool fused_possible(gcp_ctx* c);
+bool fused_use_multimem(const gcp_ctx* c);   // NVLS multicast for full-team modes
 gcp_status fused_alloc(gcp_ctx* c, size_t bytes);   // A, G, G2 as symmetric windows (collective)
 void fused_free(gcp_ctx* c);
 gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower);

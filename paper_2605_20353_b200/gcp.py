@@ -32,7 +32,8 @@ SYMBOLS = ["gcp_create", "gcp_destroy", "gcp_last_error", "gcp_grid_plan", "gcp_
            "gcp_tensor_export_sorted", "gcp_tensor_contains", "gcp_model_init", "gcp_model_set",
            "gcp_model_get", "gcp_sample", "gcp_sample_export", "gcp_loss_grad", "gcp_grad_get",
            "gcp_adam_step", "gcp_loss_estimate", "gcp_fit_begin", "gcp_fit_epoch", "gcp_fit",
-           "gcp_counters", "gcp_profile_enable", "gcp_profile_get", "gcp_set_membership"]
+           "gcp_counters", "gcp_profile_enable", "gcp_profile_get", "gcp_set_membership",
+           "gcp_dist_features"]
 MEMBERSHIP = {"hash": 0, "sorted": 1}
 
 
@@ -88,6 +89,7 @@ def load():
         "gcp_fit_epoch": [vp, dp, ip, ip],
         "gcp_fit": [vp, C.POINTER(FitParams), TRACE_FN, vp, dp],
         "gcp_counters": [vp, C.POINTER(C.c_uint32), i64p, i64p],
+        "gcp_dist_features": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "gcp_profile_enable": [vp, C.c_int],
         "gcp_profile_get": [vp, C.c_int, dp, i64p, C.c_int],
         "gcp_set_membership": [vp, C.c_int],
@@ -312,6 +314,11 @@ class Context:
         it, t, n = C.c_uint32(), C.c_int64(), C.c_int64()
         _chk(lib.gcp_counters(self.h, C.byref(it), C.byref(t), C.byref(n)), "gcp_counters")
         return dict(it=it.value, t=t.value, launches=n.value)
+
+    def dist_features(self):
+        f, m = C.c_int(), C.c_int()
+        _chk(lib.gcp_dist_features(self.h, C.byref(f), C.byref(m)), "gcp_dist_features")
+        return dict(fused=bool(f.value), multimem=bool(m.value))
 
     def profile_enable(self, on=True):
         _chk(lib.gcp_profile_enable(self.h, int(on)), "gcp_profile_enable")

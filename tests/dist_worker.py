@@ -20,6 +20,13 @@ import oracle  # noqa: E402
 
 def main():
     mode = sys.argv[1]
+    # "sync32": the sync scheme in fp32 (the fused exchange's NVLS multicast path
+    # runs in fp32 only); tolerances from DESIGN.md section 5.2
+    prec = "fp32" if mode == "sync32" else "fp64"
+    if mode == "sync32":
+        os.environ["GCP_MULTIMEM"] = "1"   # exercise the NVLS path whatever P is
+    mode = "sync" if mode == "sync32" else mode
+    TG, TM, TE = (1e-4, 1e-3, 1e-4) if prec == "fp32" else (1e-10, 1e-9, 1e-10)
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -38,7 +45,7 @@ def main():
     assert list(lo[rank]) == mine.lo and list(hi[rank]) == mine.hi
     bs, bv = mine.sorted()
 
-    ctx = g.Context(local, None, "fp64")
+    ctx = g.Context(local, None, prec)
     ctx.dist_init(ws, rank, uid[0], None, mode)
     ctx.tensor_create(dims, bs, bv)
     info = ctx.tensor_info()
@@ -46,7 +53,10 @@ def main():
     ctx.model_init(R, 77)
     A0 = oracle.factor_init(77, dims, R)
     for k in range(3):
-        assert np.array_equal(ctx.model_get(k), A0[k][mine.lo[k]:mine.hi[k]]), "init"
+        want = A0[k][mine.lo[k]:mine.hi[k]]
+        if prec == "fp32":
+            want = want.astype(np.float32).astype(np.float64)
+        assert np.array_equal(ctx.model_get(k), want), "init"
 
     tau = 2
     # the two-sided layout (row f3) computes Alg. 2 exactly like the all-reduce layout
@@ -68,7 +78,7 @@ def main():
             ctx.loss_grad(loss)
             for k in range(3):
                 Gg = ctx.grad_get(k)
-                assert np.all(np.abs(Gg - Go[k]) <= 1e-10 * S[k] + 1e-300), f"grad it={it} k={k}"
+                assert np.all(np.abs(Gg - Go[k]) <= TG * S[k] + 1e-300), f"grad it={it} k={k}"
         else:
             ctx.loss_grad(loss)
         ctx.adam_step(ap)
@@ -78,10 +88,11 @@ def main():
             got = ctx.model_get(k)
             err = np.abs(got - want).max() / max(1.0, np.abs(want).max())
             worst = max(worst, err)
-            assert err < 1e-9, f"model it={it} k={k} err={err}"
+            assert err < TM, f"model it={it} k={k} err={err}"
     est = ctx.loss_estimate(loss, 1500, 1500, 5)
     oe, sc = run.estimate(5, 1500, 1500)
-    assert abs(est - oe) <= 1e-10 * sc, (est, oe)
+    assert abs(est - oe) <= TE * sc, (est, oe)
+    feats = ctx.dist_features()
     ctx.close()
 
     # the epoch loop (R20) on a side stream: the iterations of an epoch replay
@@ -89,7 +100,7 @@ def main():
     stream = torch.cuda.Stream(local)
     uid = [g.gcp_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    ctx = g.Context(local, stream.cuda_stream, "fp64")
+    ctx = g.Context(local, stream.cuda_stream, prec)
     ctx.dist_init(ws, rank, uid[0], None, mode)
     ctx.tensor_create(dims, bs, bv)
     ctx.model_init(R, 77)
@@ -100,14 +111,15 @@ def main():
     Af, hist, obest = oracle.fit(blocks, grid, A0, loss, iters=6, mode=omode, tau=tau, meta_rate=5e-3, **kw)
     assert len(rows) == len(hist), (rows, hist)
     for r, h in zip(rows, hist):
-        assert abs(r[2] - h[0]) <= 1e-9 * abs(h[0]), (r, h)
+        assert abs(r[2] - h[0]) <= 10 * TE * abs(h[0]), (r, h)
     for k in range(3):
         want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
-        assert np.allclose(ctx.model_get(k), want, rtol=1e-8, atol=1e-10), f"fit model k={k}"
+        assert np.allclose(ctx.model_get(k), want, rtol=10 * TM, atol=TM), f"fit model k={k}"
     ctx.close()
     dist.barrier()
     if rank == 0:
-        print(f"DIST-OK mode={mode} P={ws} grid={grid} worst_model_err={worst:.2e}", flush=True)
+        print(f"DIST-OK mode={mode} prec={prec} P={ws} grid={grid} worst_model_err={worst:.2e} "
+              f"features={feats}", flush=True)
     dist.destroy_process_group()
 
 

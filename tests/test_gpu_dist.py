@@ -17,7 +17,7 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("nproc", [2, 4])
-@pytest.mark.parametrize("mode", ["sync", "twosided", "async", "fedadam"])
+@pytest.mark.parametrize("mode", ["sync", "sync32", "twosided", "async", "fedadam"])
 def test_multi_gpu_parity(mode, nproc):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
@@ -28,3 +28,4 @@ def test_multi_gpu_parity(mode, nproc):
             if "Error" in ln or "assert" in ln or "GCP_E" in ln][:20]
     assert r.returncode == 0, "\n".join(errs) + "\n" + r.stderr[-1500:]
     assert "DIST-OK" in r.stdout
+    print([ln for ln in r.stdout.splitlines() if "DIST-OK" in ln][0])

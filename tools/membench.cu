@@ -72,6 +72,27 @@ __global__ void rand_red(float4* a, uint64_t rows, int64_t total) {
     }
 }
 
+// shared-memory privatisation candidate: random 64-B rows, 4 lanes x 4 scalar
+// atomicAdd(float) each, into a per-CTA array of srows rows (dynamic smem)
+__global__ void smem_red(float* out, int srows, int64_t total) {
+    extern __shared__ float sh[];
+    for (int i = threadIdx.x; i < srows * 16; i += blockDim.x) sh[i] = 0.f;
+    __syncthreads();
+    const int lane = threadIdx.x & 3;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 2;
+    for (int64_t i = g; i < total; i += ng) {
+        const uint32_t r = __umulhi((uint32_t)mix(i), (uint32_t)srows);
+        float* p = sh + r * 16 + lane * 4;
+        atomicAdd(p, 1.f);
+        atomicAdd(p + 1, 1.f);
+        atomicAdd(p + 2, 1.f);
+        atomicAdd(p + 3, 1.f);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && sh[0] == 1.2345f) out[0] = sh[1];
+}
+
 __global__ void copy4(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = a[i];
@@ -118,6 +139,21 @@ int main() {
         printf("\"rand64_l2_rows_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
         ms = timeit([&] { rand_red<<<blocks, 256>>>(S, small / 64, total); });
         printf("\"red64_l2_rows_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+    }
+    // contention: vector red into few rows (small modes of c1 / c3)
+    for (int rows : {20, 1605, 4209, 10000}) {
+        float ms = timeit([&] { rand_red<<<sms * 8, 256>>>(S, rows, total); });
+        printf("\"red64_rows%d\": %.3e, ", rows, total / (ms * 1e-3));
+    }
+    // shared-memory scalar atomics into per-CTA rows
+    cudaFuncSetAttribute(smem_red, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int srows : {20, 1605, 3000}) {
+        for (int bps : {1, 2, 4}) {
+            const size_t sb = (size_t)srows * 64;
+            if (sb * bps > 200 * 1024) continue;
+            float ms = timeit([&] { smem_red<<<sms * bps, 256, sb>>>((float*)sink, srows, total); });
+            printf("\"smem_red64_rows%d_b%d\": %.3e, ", srows, bps, total / (ms * 1e-3));
+        }
     }
     const int64_t n4 = big / 16;
     float ms = timeit([&] { copy4<<<sms * 8, 256>>>((const float4*)A, B, n4); });
