@@ -174,12 +174,23 @@ def bcast_bytes(ws, rank, b):
 
 
 # ------------------------------------------------------------------ data
-def make_tensor(name, device):
+def make_tensor(name, device, block=None, allreduce=None):
+    """The workload's tensor; with block=(lo, hi) only this rank's block (the
+    same global tensor, generated without materialising the other blocks)."""
     w = workload(name)
     t0 = time.time()
     subs, vals = gcp_synth.chi_kolda(w["dims"], w["nnz"], w["R"], gcp_synth.SEEDS[name]["data"], w["loss"],
-                                     device=device)
+                                     device=device, block=block, allreduce=allreduce)
     return subs, vals, time.time() - t0
+
+
+def allsum_int(ws, x):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([int(x)], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t)
+    return int(t.item())
 
 
 def block_of(subs, vals, lo, hi):
@@ -288,23 +299,37 @@ def main():
     grid, lo, hi = g.gcp_grid_plan(ws, w["dims"])
 
     log("generate", name)
-    subs, vals, gen_s = make_tensor(name, f"cuda:{dev}")
+    if ws > 1 and w["nnz"] > 1_000_000_000:
+        # billion-scale: each rank generates only its block of the global tensor
+        subs, vals, gen_s = make_tensor(name, f"cuda:{dev}", block=(lo[rank], hi[rank]),
+                                        allreduce=lambda x: allsum_int(ws, x))
+    else:
+        subs, vals, gen_s = make_tensor(name, f"cuda:{dev}")
+        if ws > 1:
+            subs, vals = block_of(subs, vals, lo[rank], hi[rank])
     log("generated", len(vals))
-    if ws > 1:
-        subs, vals = block_of(subs, vals, lo[rank], hi[rank])
-    subs_h = torch.empty(subs.shape, dtype=subs.dtype, pin_memory=True)
-    subs_h.copy_(subs)
-    del subs
-    vals_h = torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True)
-    vals_h.copy_(vals)
-    del vals
-    log("host copy (pinned)")
+    device_ingest = args.no_e2e and w["nnz"] > 1_000_000_000 and ws > 1
+    if device_ingest:
+        # billion-scale block without e2e: ingest straight from the generated
+        # device arrays (the ABI takes any UVA pointer), no host copy
+        subs_h, vals_h = subs, vals
+    else:
+        subs_h = torch.empty(subs.shape, dtype=subs.dtype, pin_memory=True)
+        subs_h.copy_(subs)
+        vals_h = torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True)
+        vals_h.copy_(vals)
+        log("host copy (pinned)")
+    del subs, vals
     nnz_local = len(vals_h)
     torch.cuda.empty_cache()
     t0 = time.time()
     log("ingest", nnz_local)
     ctx.tensor_create_ptr(w["dims"], nnz_local, subs_h.data_ptr(), vals_h.data_ptr())
     ingest_s = time.time() - t0
+    if device_ingest:
+        del subs_h, vals_h
+        subs_h = vals_h = None
+        torch.cuda.empty_cache()
     ctx.model_init(w["R"], gcp_synth.SEEDS[name]["model"])
     features = ctx.dist_features()
     fp = ctx.fit_params(epochs=10 ** 6, iters_per_epoch=ITERS, max_fails=10 ** 6, s_nz=w["s"], s_z=w["s"],

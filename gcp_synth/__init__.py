@@ -79,13 +79,21 @@ def _merge2(hi, lo, cnt):
 
 
 def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, boost=10.0,
-              tol=0.005, max_rounds=64, force_wide=False):
+              tol=0.005, max_rounds=64, force_wide=False, block=None, allreduce=None):
     """Return (subs int64 [N, d], vals float64 [N]) as torch tensors on `device`.
 
     Duplicate draws merge on an int64 mixed-radix key when prod(dims) < 2^62,
-    else on the pair (i_1, key of the other modes) (needs prod(dims[1:]) < 2^63)."""
+    else on the pair (i_1, key of the other modes) (needs prod(dims[1:]) < 2^63).
+
+    block = (lo, hi): keep only the entries with lo_k <= i_k < hi_k (one rank's
+    block of a medium-grained grid) without materialising the rest.  Every rank
+    consumes the identical draw stream, so the blocks of all ranks partition the
+    one global tensor; `allreduce(int) -> int` sums the kept distinct counts over
+    the ranks, so the top-up test sees the global count.  Only the rare thinning
+    step (an overshoot beyond nnz * (1 + tol)) and the shuffle order then depend
+    on the block."""
     dims = [int(i) for i in dims]
-    wide = force_wide or math.prod(dims) >= 2 ** 62
+    wide = force_wide or block is not None or math.prod(dims) >= 2 ** 62
     assert not wide or math.prod(dims[1:]) < 2 ** 63
     assert nnz <= math.prod(dims)
     g = _gen(seed, device)
@@ -134,8 +142,9 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
         # Billion-scale path: draws arrive in rounds of <= 4e8 and are split into
         # i_1-range partitions (duplicates share i_1) of < 2^31 entries each, so
         # every sort stays below 2^31 elements.
+        blo, bhi = (list(block[0]), list(block[1])) if block is not None else ([0] * len(dims), dims)
         nparts = max(1, -(-nnz // 200_000_000))
-        edges = [dims[0] * j // nparts for j in range(nparts + 1)]
+        edges = [int(blo[0]) + (int(bhi[0]) - int(blo[0])) * j // nparts for j in range(nparts + 1)]
         parts = [(torch.empty(0, dtype=torch.int64, device=device),) * 3 for _ in range(nparts)]
         total = 0
         for _ in range(max_rounds):
@@ -144,6 +153,12 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
                 n_draw = min(left, 400_000_000)
                 left -= n_draw
                 cols = _draw(cdfs, dims, R, n_draw, g, device)
+                if block is not None:
+                    m = torch.ones(n_draw, dtype=torch.bool, device=device)
+                    for k in range(len(dims)):
+                        m &= (cols[k] >= int(blo[k])) & (cols[k] < int(bhi[k]))
+                    cols = [c[m] for c in cols]
+                    del m
                 nlo = cols[1].clone()
                 for k in range(2, len(dims)):
                     nlo = nlo * dims[k] + cols[k]
@@ -157,6 +172,8 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
                                        torch.cat([pc, torch.ones(int(m.sum()), dtype=torch.int64, device=device)]))
                 del nhi, nlo, pid
             total = sum(p[0].numel() for p in parts)
+            if allreduce is not None:
+                total = int(allreduce(total))
             if total >= lo_target:
                 break
         keep = nnz / total if total > nnz * (1 + tol) else None

@@ -154,8 +154,10 @@ gcp_status gcp_dist_set_async(gcp_ctx* ctx, int64_t tau, const gcp_adam_params* 
 /* ---- tensor (row a0) -------------------------------- */
 
 /* Ingest this rank's nonzeros: 2 <= d <= 6 modes of global sizes dims[d] (each in
- * [1, 2^32-1]); subs = nnz*d int64 GLOBAL coordinates, row-major (host,
- * pageable or pinned); vals = nnz doubles (finite; 0.0 allowed, reading R26).
+ * [1, 2^32-1]); subs = nnz*d int64 GLOBAL coordinates, row-major; vals = nnz
+ * doubles (finite; 0.0 allowed, reading R26).  Both borrowed for the call:
+ * host memory (pageable or pinned) or device memory of this context's GPU
+ * (copied in chunks with cudaMemcpyDefault, i.e. any UVA pointer).
  * For nranks > 1 every nonzero must lie in this rank's block.  The device sorts
  * the nonzeros lexicographically (i_1 most significant, reading R15), rejects
  * duplicates, and builds the hash set of block-linearised keys (u64, or u128

@@ -240,8 +240,8 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
         CK(gmalloc(c, &d_vc, (size_t)chunk * 8));
         for (int64_t b = 0; b < nnz; b += chunk) {
             const int64_t n = std::min(chunk, nnz - b);
-            CK(cudaMemcpyAsync(d_sc, subs_h + b * d, (size_t)n * d * 8, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_vc, vals_h + b, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_sc, subs_h + b * d, (size_t)n * d * 8, cudaMemcpyDefault, st));
+            CK(cudaMemcpyAsync(d_vc, vals_h + b, (size_t)n * 8, cudaMemcpyDefault, st));
             k_convert<T, PermT><<<nb, 256, 0, st>>>(ka, b, n, d_sc, d_vc, coords, valt, k0, h0, p0, d_flags);
             CK(cudaGetLastError());
             c->launches++;

@@ -46,3 +46,46 @@ def test_wide_shape_lbnl_like():
     assert (v == 1).all() and abs(len(v) - 5000) <= 25
     rows = {tuple(r) for r in s.tolist()}
     assert len(rows) == len(v)
+
+
+def test_block_generation_partitions_the_global_tensor():
+    """Per-rank block generation (bench at N > 1): four concurrent 'ranks' of a
+    2x1x2 grid, summing their kept counts through a barrier-based allreduce,
+    reproduce exactly the blocks of the whole tensor (tolerance band wide
+    enough that nothing is thinned)."""
+    import threading
+    dims = (300, 200, 100)
+    full = gcp_synth.chi_kolda(dims, 20000, 4, 3, tol=0.05, force_wide=True)
+    blocks = [([0, 0, 0], [150, 200, 50]), ([0, 0, 50], [150, 200, 100]),
+              ([150, 0, 0], [300, 200, 50]), ([150, 0, 50], [300, 200, 100])]
+    bar = threading.Barrier(4)
+    slots, out = [0] * 4, [None] * 4
+
+    def rank(w):
+        def allreduce(x):
+            slots[w] = x
+            bar.wait()
+            t = sum(slots)
+            bar.wait()
+            return t
+        out[w] = gcp_synth.chi_kolda(dims, 20000, 4, 3, tol=0.05, block=blocks[w], allreduce=allreduce)
+
+    th = [threading.Thread(target=rank, args=(w,)) for w in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+
+    def canon(s, v):
+        key = (s[:, 0] * 200 + s[:, 1]) * 100 + s[:, 2]
+        o = torch.argsort(key)
+        return key[o], v[o]
+    fs, fv = full
+    for w, (lo, hi) in enumerate(blocks):
+        m = torch.ones(len(fv), dtype=torch.bool)
+        for k in range(3):
+            m &= (fs[:, k] >= lo[k]) & (fs[:, k] < hi[k])
+        kf, vf = canon(fs[m], fv[m])
+        kb, vb = canon(*out[w])
+        assert torch.equal(kf, kb) and torch.equal(vf, vb), w
+    assert sum(len(o[1]) for o in out) == len(fv)
