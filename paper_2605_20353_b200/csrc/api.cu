@@ -162,6 +162,8 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     s.N = c->N;
     s.hash = c->d_hash;
     s.hash_mask = c->hash_slots - 1;
+    s.filter = c->filter_sectors ? c->d_filter : nullptr;
+    s.filter_mask = c->filter_sectors ? c->filter_sectors - 1 : 0;
     s.key128 = c->key128;
     for (int k = 0; k < kMaxModes; ++k) s.bdim[k] = k < c->d ? (uint32_t)(c->hi[k] - c->lo[k]) : 1u;
     s.p = p;
@@ -354,6 +356,7 @@ void gcp_destroy(gcp_ctx* c) {
     gfree(c, c->d_rec);
     gfree(c, c->d_hash);
     gfree(c, c->d_keys);
+    gfree(c, c->d_filter);
     gfree(c, c->d_partials);
     gfree(c, c->d_err);
     gfree(c, c->d_step);

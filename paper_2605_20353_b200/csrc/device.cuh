@@ -48,6 +48,24 @@ __device__ __forceinline__ uint64_t hash_key(uint64_t lo, uint64_t hi) { return 
 
 constexpr uint64_t kEmpty = ~0ull;
 
+// Blocked Bloom filter in front of the exact zero test: a key owns one 32-byte
+// sector (4 u64 words) and sets one bit in each word.  Sized to stay in L2
+// (ingest.cu); a zero candidate reads its sector instead of a DRAM bucket and
+// runs the exact test (hash probe or row f4's O(log N) search) only on
+// "maybe".  No false negatives.  In front of the sorted search it is used
+// from 4 bits per key (c2: 5.4 bits, ~8% false positives, f4 K2 3x faster); in
+// front of the hash only from 12 bits per key (< 1% false positives), since a
+// "maybe" stalls its warp on a synchronous probe (profiles/r01_summary.md).
+__device__ __forceinline__ uint64_t filter_hash(uint64_t klo, uint64_t khi) {
+    return mix64(hash_key(klo, khi) ^ 0x5851F42D4C957F2Dull);
+}
+__device__ __forceinline__ bool filter_maybe(const uint4& w0, const uint4& w1, uint64_t fh) {
+    const uint64_t q0 = ((uint64_t)w0.y << 32) | w0.x, q1 = ((uint64_t)w0.w << 32) | w0.z;
+    const uint64_t q2 = ((uint64_t)w1.y << 32) | w1.x, q3 = ((uint64_t)w1.w << 32) | w1.z;
+    return ((q0 >> ((fh >> 32) & 63)) & (q1 >> ((fh >> 38) & 63)) & (q2 >> ((fh >> 44) & 63)) &
+            (q3 >> ((fh >> 50) & 63)) & 1ull) != 0;
+}
+
 // Bucketised linear probing: a key hashes to a 32-byte bucket (4 u64 slots or
 // 2 u128 slots); insertion and lookup scan slots from the bucket start, so an
 // empty slot proves absence.  One 32-B sector per probe at load <= 0.5.
@@ -130,7 +148,8 @@ struct Pending {
     uint4 w0, w1;        // record words / bucket words as loaded
     uint32_t c[D];       // zero candidate (attempt 0)
     uint32_t slot;       // local slot within the stratum
-    int state;           // 0 invalid, 1 nonzero, 2 zero (probe pending), 3 zero (no probe)
+    int state;           // 0 invalid, 1 nonzero, 2 zero (bucket loaded), 3 zero (no probe needed),
+                         // 4 zero (sorted search at resolve), 5 zero (filter sector loaded)
     uint32_t j;          // nonzero index (low 32 bits; high bits recomputed if N >= 2^32)
 };
 
@@ -191,12 +210,19 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
         P.state = 3;
         return P;
     }
+    uint64_t klo, khi;
+    const uint64_t b = first_bucket<D>(a, P.c, klo, khi);
+    if (a.filter) {          // the filter sector (L2); the exact test only on "maybe"
+        const uint4* f = reinterpret_cast<const uint4*>(a.filter + 4 * (filter_hash(klo, khi) & a.filter_mask));
+        P.w0 = __ldg(f);
+        P.w1 = __ldg(f + 1);
+        P.state = 5;
+        return P;
+    }
     if (a.member_sorted) {   // row f4: O(log N) search of the sorted keys at resolve time
         P.state = 4;
         return P;
     }
-    uint64_t klo, khi;
-    const uint64_t b = first_bucket<D>(a, P.c, klo, khi);
     const uint4* h = reinterpret_cast<const uint4*>(a.hash + b);
     P.w0 = __ldg(h);
     P.w1 = __ldg(h + 1);
@@ -270,13 +296,16 @@ __device__ __forceinline__ Sample<T, D> resolve_sample(const SampleArgs& a, cons
     o.attempts = 1;
 #pragma unroll
     for (int k = 0; k < D; ++k) o.c[k] = P.c[k];
-    if (P.state != 2 && P.state != 4) return o;
-    // zero candidate: decide attempt 0 from the prefetched bucket (or the sorted
-    // search); rejected candidates redraw all d indices -- rare, inline
+    if (P.state != 2 && P.state != 4 && P.state != 5) return o;
+    // zero candidate: decide attempt 0 from the prefetched bucket (or the filter
+    // sector + sorted search); rejected candidates redraw all d indices
+    // -- rare, inline
     uint64_t klo, khi;
     first_bucket<D>(a, o.c, klo, khi);
     bool present;
-    if (P.state == 4) {
+    if (P.state == 5) {
+        present = filter_maybe(P.w0, P.w1, filter_hash(klo, khi)) && probe_from(a, klo, khi);
+    } else if (P.state == 4) {
         present = sorted_contains(a, klo, khi);
     } else {
         const int v = bucket_verdict(a, P.w0, P.w1, klo, khi);

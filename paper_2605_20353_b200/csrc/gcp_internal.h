@@ -52,6 +52,8 @@ struct SampleArgs {
     const uint64_t* keys;     // sorted block keys (u64, or (lo,hi) pairs for u128)
     unsigned long long* err_slot;  // min zero slot that hit the rejection cap (ULLONG_MAX = none)
     const uint32_t* it_dev;   // non-null inside a captured epoch graph: it = *it_dev + it (offset)
+    const uint64_t* filter;   // blocked Bloom filter of the block's keys (4 u64 per 32-B sector), or null
+    uint64_t filter_mask;     // sectors - 1 (power of two)
 };
 
 // Epoch-graph replay state: the values of rate, t and it at the start of the
@@ -129,6 +131,8 @@ struct gcp_ctx {
     int key128 = 0;
     gcp_membership member = GCP_MEMBER_HASH;   // zero-test structure built at ingest
     uint64_t* d_keys = nullptr;                // sorted keys (GCP_MEMBER_SORTED)
+    uint64_t* d_filter = nullptr;              // L2-resident negative test in front of the zero test
+    uint64_t filter_sectors = 0;
     // ---- model
     bool have_model = false;
     int R = 0, R_pad = 0;

@@ -130,6 +130,35 @@ __global__ void k_hash_insert(int64_t n, const uint64_t* __restrict__ klo, const
     }
 }
 
+// blocked Bloom filter (device.cuh filter_maybe): one bit in each u64 of the key's sector
+__global__ void k_filter_insert(int64_t n, const uint64_t* __restrict__ klo, const uint64_t* __restrict__ khi,
+                                unsigned long long* __restrict__ f, uint64_t mask) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t fh = filter_hash(klo[x], khi ? khi[x] : 0);
+        unsigned long long* sec = f + 4 * (fh & mask);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) atomicOr(sec + i, 1ull << ((fh >> (32 + 6 * i)) & 63));
+    }
+}
+
+// Filter size: ~16 bits per key in a power-of-two number of 32-B sectors,
+// capped at min(64 MB, 0.55 L2) so it stays L2-resident next to the factors;
+// off below min_bits per key (4 in front of the sorted search, 12 in front of
+// the hash: c2 keeps the plain hash, c4/c5 have no filter at all).
+// GCP_FILTER=0 disables it, GCP_FILTER_MB sets the cap.
+static uint64_t filter_sectors_for(const gcp_ctx* c, int64_t nnz, int min_bits) {
+    const char* env = getenv("GCP_FILTER");
+    if ((env && std::string(env) == "0") || nnz <= 0) return 0;
+    const char* mb = getenv("GCP_FILTER_MB");
+    const double cap_mb = mb ? atof(mb) : 64.0;
+    const uint64_t cap = std::min<uint64_t>((uint64_t)(cap_mb * 1048576.0), (uint64_t)(c->l2_bytes * 0.55));
+    const uint64_t want = (uint64_t)nnz * 2;
+    uint64_t bytes = 32;
+    while (bytes < want && bytes * 2 <= cap) bytes <<= 1;
+    if (bytes * 8 < (uint64_t)nnz * min_bits) return 0;
+    return bytes / 32;
+}
+
 // sorted key array for the binary-search zero test (row f4): u64, or (lo, hi) pairs
 __global__ void k_store_keys(int64_t n, const uint64_t* __restrict__ klo, const uint64_t* __restrict__ khi,
                              uint64_t* __restrict__ out) {
@@ -226,6 +255,8 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
     uint32_t* new_rec = nullptr;
     uint64_t* new_hash = nullptr;
     uint64_t* new_keys = nullptr;
+    uint64_t* new_filter = nullptr;
+    const uint64_t fsect = filter_sectors_for(c, nnz, sorted_member ? 4 : 12);
 
     CK(gmalloc(c, &d_flags, sizeof(unsigned)));
     CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
@@ -319,6 +350,13 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
         else k_hash_insert<<<nb, 256, 0, st>>>(nnz, skl, skh, new_hash, slots - 1);
         CK(cudaGetLastError());
         c->launches++;
+        if (fsect) {
+            CK(gmalloc(c, &new_filter, (size_t)fsect * 32));
+            CK(cudaMemsetAsync(new_filter, 0, (size_t)fsect * 32, st));
+            k_filter_insert<<<nb, 256, 0, st>>>(nnz, skl, skh, (unsigned long long*)new_filter, fsect - 1);
+            CK(cudaGetLastError());
+            c->launches++;
+        }
     }
     CK(cudaStreamSynchronize(st));
 
@@ -329,6 +367,7 @@ cleanup:
         gfree(c, new_rec);
         gfree(c, new_hash);
         gfree(c, new_keys);
+        gfree(c, new_filter);
         if (err == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             return set_error(GCP_E_OOM, "gcp_tensor_create: out of device memory");
@@ -340,6 +379,9 @@ cleanup:
     gfree(c, c->d_rec);
     gfree(c, c->d_hash);
     gfree(c, c->d_keys);
+    gfree(c, c->d_filter);
+    c->d_filter = new_filter;
+    c->filter_sectors = new_filter ? fsect : 0;
     c->d_rec = new_rec;
     c->d_hash = new_hash;
     c->d_keys = new_keys;

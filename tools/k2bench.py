@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--l2fetch", default="", help="comma list of cudaLimitMaxL2FetchGranularity values to sweep")
+    ap.add_argument("--strategies", default="stratified", help="comma list: stratified,semi")
+    ap.add_argument("--membership", default="hash", help="hash or sorted (row f4)")
     args = ap.parse_args()
     import paper_2605_20353_b200 as g
     c = gcp_synth.CONFIGS[args.config]
@@ -39,6 +41,7 @@ def main():
     torch.cuda.empty_cache()
     stream = torch.cuda.Stream()
     ctx = g.Context(0, stream.cuda_stream, args.precision)
+    ctx.set_membership(args.membership)
     t0 = time.time()
     ctx.tensor_create_ptr(c["dims"], vals_h.numel(), subs_h.data_ptr(), vals_h.data_ptr())
     t_ingest = time.time() - t0
@@ -49,7 +52,8 @@ def main():
         ctx.adam_step()
     ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
     sweep = [int(x) for x in args.l2fetch.split(",")] if args.l2fetch else [None]
-    for l2f in sweep:
+    for strat, l2f in [(st, l) for st in args.strategies.split(",") for l in sweep]:
+        ctx.sample(strat, c["s"], c["s"], s["sample"])
         if l2f is not None:   # device-wide hint through the process's CUDA runtime
             import ctypes
             rt = ctypes.CDLL("libcudart.so.12")
@@ -62,7 +66,7 @@ def main():
             ctx.adam_step()
         for _ in range(3):
             ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
-        out = {"config": args.config, "L2_FETCH": l2f if l2f is not None else os.environ.get("GCP_L2_FETCH", "32"),
+        out = {"config": args.config, "strategy": strat, "membership": args.membership, "L2_FETCH": l2f if l2f is not None else os.environ.get("GCP_L2_FETCH", "32"),
                "ingest_s": t_ingest}
         for k in ("grad", "adam", "loss"):
             ms, n = ctx.profile_get(k)

@@ -93,6 +93,46 @@ __global__ void smem_red(float* out, int srows, int64_t total) {
     if (threadIdx.x == 0 && sh[0] == 1.2345f) out[0] = sh[1];
 }
 
+// K2's memory skeleton per sample (no Philox, no hash logic): optionally one
+// random 16-B DRAM load (record / bucket), then 3 random 64-B row loads and 3
+// random 64-B red.add.v4 rows in an L2-resident factor / gradient array, 4
+// lanes per sample -- the combined L2 ceiling the fused kernel shares.
+__global__ void k2_skeleton(const uint4* __restrict__ big, uint64_t nbig, const float4* __restrict__ A, float4* G,
+                            uint64_t rows, int64_t total, int with_dram, float* sink) {
+    const int lane = threadIdx.x & 3;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 2;
+    float acc = 0.f;
+    for (int64_t i = g; i < total; i += ng) {
+        uint64_t h = mix(i);
+        uint32_t extra = 0;
+        if (with_dram) {
+            const uint4 v = __ldg(big + __umul64hi(h, nbig));
+            extra = v.x & 1;
+        }
+        uint64_t r[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            h = mix(h + k + 1 + extra);
+            r[k] = __umul64hi(h, rows / 3) + k * (rows / 3);
+        }
+        float4 a[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a[k] = __ldg(A + r[k] * 4 + lane);
+        const float m = a[0].x * a[1].x * a[2].x + a[0].y * a[1].y * a[2].y;
+        acc += m;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float* p = reinterpret_cast<float*>(G + r[k] * 4 + lane);
+            const float4 o = a[(k + 1) % 3], q = a[(k + 2) % 3];
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(m * o.x * q.x),
+                         "f"(m * o.y * q.y), "f"(m * o.z * q.z), "f"(m * o.w * q.w)
+                         : "memory");
+        }
+    }
+    if (acc == 1.2345f) *sink = acc;
+}
+
 __global__ void copy4(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = a[i];
@@ -154,6 +194,20 @@ int main() {
             float ms = timeit([&] { smem_red<<<sms * bps, 256, sb>>>((float*)sink, srows, total); });
             printf("\"smem_red64_rows%d_b%d\": %.3e, ", srows, bps, total / (ms * 1e-3));
         }
+    }
+    // K2 skeleton on c2's shape: 30,000 rows of 64 B per array (A and G 1.9 MB), 2e7 samples
+    {
+        float4* G2;
+        cudaMalloc(&G2, small);
+        cudaMemset(G2, 0, small);
+        const int64_t ns = 20000000;
+        for (int wd : {0, 1}) {
+            for (int blocks : {sms * 4, sms * 8}) {
+                float ms = timeit([&] { k2_skeleton<<<blocks, 256>>>(A, big / 16, S, G2, 30000, ns, wd, (float*)sink); });
+                printf("\"k2skel_dram%d_b%d_ms_per_2e7\": %.4f, ", wd, blocks, ms);
+            }
+        }
+        cudaFree(G2);
     }
     const int64_t n4 = big / 16;
     float ms = timeit([&] { copy4<<<sms * 8, 256>>>((const float4*)A, B, n4); });
