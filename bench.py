@@ -416,6 +416,8 @@ def main():
                                  else "and gradient far exceed L2")),
                        "nnz_local_rank0": nnz_local},
             "samples_per_s": samples_per_s,
+            # all ranks' K2 run concurrently: global samples per iteration / the slowest rank's K2
+            "samples_per_s_k2_only": 2 * w["s"] / (k2_avg_ms * 1e-3) if k2_avg_ms else None,
             "hbm_gbs_k2_algorithmic": achieved,
             "gpu_launches": int(launches),
             "library_launches_total": int(c1["launches"] - c0["launches"]),

@@ -328,3 +328,30 @@ def test_fit_runs_and_decreases(gcp, orc):
     assert best < F0
     ests = [r[2] for r in rows]
     assert min(ests) == pytest.approx(best)
+
+
+@pytest.mark.parametrize("membership", ["hash", "sorted"])
+def test_filter_leaves_samples_unchanged(gcp, monkeypatch, membership):
+    """The L2 Bloom filter in front of the zero test is a pure accelerator: with
+    and without it (GCP_FILTER=1/0 at ingest) the zero samples, their
+    attempt counts (c1 is dense: rejections happen) and the gradient agree
+    bit for bit (gradient: same samples, same kernel; fp64 so atomics order
+    cannot blur a difference at this size)."""
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    out = []
+    for f in ("1", "0"):
+        monkeypatch.setenv("GCP_FILTER", f)
+        c = gcp.Context(0, None, "fp64")
+        c.set_membership(membership)
+        c.tensor_create(dims, subs, vals)
+        c.model_init(4, 2001)
+        c.sample("stratified", 500, 3000, 77)
+        gs, _, _, ga = c.sample_export(1, 0, 3000)
+        c.loss_grad("poisson")
+        out.append((gs, ga, [c.grad_get(k) for k in range(3)]))
+        c.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][1].max() > 1   # rejections exercised
+    for k in range(3):
+        assert np.allclose(out[0][2][k], out[1][2][k], rtol=1e-12, atol=1e-12)
