@@ -133,6 +133,40 @@ __global__ void k2_skeleton(const uint4* __restrict__ big, uint64_t nbig, const 
     if (acc == 1.2345f) *sink = acc;
 }
 
+// c4-shaped skeleton: factor rows DRAM-resident, A and G rows interleaved in
+// one 128-B line (row r: A at float4 8r..8r+3, G at 8r+4..8r+7), 3 modes.
+__global__ void k2_skeleton_dram(const uint4* __restrict__ big, uint64_t nbig, float4* AG, uint64_t rows,
+                                 int64_t total, float* sink) {
+    const int lane = threadIdx.x & 3;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 2;
+    float acc = 0.f;
+    for (int64_t i = g; i < total; i += ng) {
+        uint64_t h = mix(i);
+        const uint4 v = __ldg(big + __umul64hi(h, nbig));
+        uint64_t r[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            h = mix(h + k + 1 + (v.x & 1));
+            r[k] = __umul64hi(h, rows / 3) + k * (rows / 3);
+        }
+        float4 a[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a[k] = __ldg(AG + r[k] * 8 + lane);
+        const float m = a[0].x * a[1].x * a[2].x + a[0].y * a[1].y * a[2].y;
+        acc += m;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float* p = reinterpret_cast<float*>(AG + r[k] * 8 + 4 + lane);
+            const float4 o = a[(k + 1) % 3], q = a[(k + 2) % 3];
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(m * o.x * q.x),
+                         "f"(m * o.y * q.y), "f"(m * o.z * q.z), "f"(m * o.w * q.w)
+                         : "memory");
+        }
+    }
+    if (acc == 1.2345f) *sink = acc;
+}
+
 __global__ void copy4(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = a[i];
@@ -208,6 +242,18 @@ int main() {
             }
         }
         cudaFree(G2);
+    }
+    // c4-shaped skeleton: 8.4M rows x 128 B (A|G interleaved, 1.07 GB), 2e7 samples
+    {
+        const uint64_t rows4 = 8400000;
+        float4* AG;
+        cudaMalloc(&AG, rows4 * 128);
+        cudaMemset(AG, 0, rows4 * 128);
+        for (int blocks : {sms * 4, sms * 8}) {
+            float ms = timeit([&] { k2_skeleton_dram<<<blocks, 256>>>(A, big / 16, AG, rows4, 20000000, (float*)sink); });
+            printf("\"k2skel_c4_b%d_ms_per_2e7\": %.4f, ", blocks, ms);
+        }
+        cudaFree(AG);
     }
     const int64_t n4 = big / 16;
     float ms = timeit([&] { copy4<<<sms * 8, 256>>>((const float4*)A, B, n4); });
