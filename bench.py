@@ -449,9 +449,18 @@ def random_access_bound(w, p_loc, k2_ms):
     DRAM load per sample in one kernel: they share the L2); otherwise the larger
     of the scatter-add, gather and DRAM times alone."""
     f = ROOT / "profiles" / "membench_r01.json"
-    if not f.exists() or w["R"] * 4 != 64 or sum(w["dims"]) * w["R"] * 4 > 32e6:
+    if not f.exists() or w["R"] * 4 != 64:
         return None
     m = json.loads(f.read_text())
+    if sum(w["dims"]) * w["R"] * 4 > 32e6:
+        # factors DRAM-resident (c4): the measured c4-shaped skeleton (A|G rows
+        # interleaved in 128-B lines, one random DRAM load + 3 gathers + 3 red.add per sample)
+        if w["d"] != 3 or "k2_skeleton_c4_ms_per_2e7" not in m:
+            return None
+        bound = m["k2_skeleton_c4_ms_per_2e7"] * 2 * p_loc / 2e7
+        return {"bound": "hbm-random-composite", "ceiling_ms": bound, "achieved_ms": k2_ms, "frac": bound / k2_ms,
+                "parts_ms": {"composite_skeleton": bound},
+                "source": "profiles/membench_r01.json (tools/membench.cu k2_skeleton_dram)"}
     n = 2 * p_loc
     t_red = w["d"] * n / m["red64_rows_l2_per_s"] * 1e3
     t_gather = w["d"] * n / m["rand64_rows_l2_per_s"] * 1e3
