@@ -1,9 +1,11 @@
-"""Full-size parity on BASELINE config c2 (10K^3, 1e8 nnz, R=16, Poisson,
-p = q = 1e7) in the launch configuration bench.py times: sampled slots are
-compared bit-exactly (first 1e5 slots of each stratum + 1e5 random slots),
-the full-size gradient element-wise against the oracle's fp64 fused
-sampling-MTTKRP over all 2e7 samples, and the loss estimate at f = 1e7.
-Heavy (about 2-3 minutes of oracle host time)."""
+"""Full-size parity on BASELINE configs c2 (10K^3, 1e8 nnz, R=16, Poisson,
+p = q = 1e7) and c3 (5-way LBNL-shaped, 1.7e6 nnz, u128 keys, R=10,
+Bernoulli, p = q = 1e6; the L2 Bloom filter is in front of its hash) in the
+launch configuration bench.py times: sampled slots are compared bit-exactly
+(first 1e5 slots of each stratum + 1e5 random slots), the full-size gradient
+element-wise against the oracle's fp64 fused sampling-MTTKRP over all p + q
+samples, and the loss estimate at the config's f.  Heavy (about 2-3 minutes of
+oracle host time for c2)."""
 import numpy as np
 import pytest
 import torch
@@ -13,10 +15,10 @@ import gcp_synth
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def c2(orc):
+@pytest.fixture(scope="module", params=["c2", "c3"])
+def full(orc, request):
     import paper_2605_20353_b200 as g
-    cfg, seeds = gcp_synth.CONFIGS["c2"], gcp_synth.SEEDS["c2"]
+    cfg, seeds = gcp_synth.CONFIGS[request.param], gcp_synth.SEEDS[request.param]
     subs, vals = gcp_synth.chi_kolda(cfg["dims"], cfg["nnz"], cfg["R"], seeds["data"], cfg["loss"], device="cuda")
     subs_h, vals_h = subs.cpu().numpy(), vals.cpu().numpy()
     del subs, vals
@@ -24,13 +26,16 @@ def c2(orc):
     ctx = g.Context(0, None, "fp32")
     ctx.tensor_create(cfg["dims"], subs_h, vals_h)
     ctx.model_init(cfg["R"], seeds["model"])
+    if cfg["loss"] == "bernoulli":   # centre the model so sigma(m) is not saturated (as the parity tests do)
+        for k in range(len(cfg["dims"])):
+            ctx.model_set(k, ctx.model_get(k) - 0.5)
     ctx.sample("stratified", cfg["s"], cfg["s"], seeds["sample"])
     t = orc.Tensor(cfg["dims"], subs_h, vals_h)
     return ctx, t, cfg, seeds
 
 
-def test_c2_sample_indices_bit_exact(orc, c2):
-    ctx, t, cfg, seeds = c2
+def test_full_size_sample_indices_bit_exact(orc, full):
+    ctx, t, cfg, seeds = full
     p = cfg["s"]
     rng = np.random.default_rng(0)
     for stratum in (0, 1):
@@ -44,13 +49,14 @@ def test_c2_sample_indices_bit_exact(orc, c2):
             assert np.array_equal(gs, os_) and np.array_equal(gj, oj) and np.array_equal(ga, oa)
 
 
-def test_c2_full_gradient_and_loss_estimate(orc, c2):
-    ctx, t, cfg, seeds = c2
-    A = [ctx.model_get(k) for k in range(3)]
+def test_full_size_gradient_and_loss_estimate(orc, full):
+    ctx, t, cfg, seeds = full
+    d = len(cfg["dims"])
+    A = [ctx.model_get(k) for k in range(d)]
     ctx.loss_grad(cfg["loss"])
-    G = [ctx.grad_get(k) for k in range(3)]
+    G = [ctx.grad_get(k) for k in range(d)]
     Go, S, _ = orc.sampled_grad(t, A, cfg["loss"], seeds["sample"], 0, 0, cfg["s"], cfg["s"])
-    for k in range(3):
+    for k in range(d):
         diff = np.abs(G[k] - Go[k])
         assert (diff <= 1e-4 * S[k]).all(), f"mode {k}: worst {(diff / S[k]).max():.2e}"
         assert np.linalg.norm(G[k] - Go[k]) <= 1e-4 * np.linalg.norm(Go[k])
