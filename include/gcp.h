@@ -187,7 +187,8 @@ gcp_status gcp_tensor_contains(gcp_ctx* ctx, int64_t n, const int64_t* coords, i
 
 /* ---- model (Eq. CP, P:257-263 with lambda) -------------------------- */
 
-/* Allocate rank-R factors for this rank's block rows, moments B = C = 0 and
+/* Allocate rank-R factors (1 <= R <= 128 in fp32, 64 in fp64; rows padded to
+ * a multiple of 4 columns) for this rank's block rows, moments B = C = 0 and
  * the gradient G = 0 (one contiguous array each), lambda = 1, and
  * fill A^(k) ~ U[0,1) by Philox (reading R12; identical on every rank and for
  * every grid).  Resets the Adam step t and the iteration counter to 0. */

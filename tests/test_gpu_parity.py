@@ -355,3 +355,46 @@ def test_filter_leaves_samples_unchanged(gcp, monkeypatch, membership):
     assert out[0][1].max() > 1   # rejections exercised
     for k in range(3):
         assert np.allclose(out[0][2][k], out[1][2][k], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("prec,R", [("fp32", 3), ("fp32", 7), ("fp32", 13), ("fp32", 32), ("fp32", 50),
+                                    ("fp32", 128), ("fp64", 2), ("fp64", 8), ("fp64", 24), ("fp64", 64)])
+def test_gradient_parity_row_geometries(gcp, orc, prec, R):
+    """Every lane geometry of K2 (GL lanes x NV 16-B vectors per row: 1x1 ...
+    8x4) against the oracle, up to the largest R the ABI accepts."""
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals, prec=prec, R=R)
+    t = orc.Tensor(dims, subs, vals)
+    c.sample("stratified", 600, 600, 3001)
+    A = _model(c, 3)
+    c.loss_grad("poisson")
+    G = [c.grad_get(k) for k in range(3)]
+    Go, S, _ = orc.sampled_grad(t, A, "poisson", 3001, 0, 0, 600, 600)
+    _grad_check(G, Go, S, TOL[prec] * (10 if prec == "fp32" and R > 32 else 1), f"R={R}/{prec}")
+    est = c.loss_estimate("poisson", 1500, 1500, 4001)
+    oe, scale = orc.loss_estimate(t, A, "poisson", 4001, 0, 1500, 1500)
+    assert abs(est - oe) <= TOL[prec] * scale * (10 if R > 32 else 1)
+
+
+@pytest.mark.parametrize("dims", [(60, 70), (9, 10, 11, 12), (4, 5, 6, 5, 4, 6)])
+def test_gradient_parity_orders(gcp, orc, dims):
+    """Tensor orders d = 2, 4, 6 (d = 3 and 5 above): ingest order, sample
+    indices and the gradient."""
+    subs, vals = gcp_synth.chi_kolda(dims, 1500, 3, 1007, loss="gaussian")
+    subs, vals = subs.numpy(), vals.numpy() - 1.0
+    c = _ctx(gcp, dims, subs, vals, prec="fp64", R=5)
+    t = orc.Tensor(dims, subs, vals)
+    ss, sv = t.sorted()
+    gs, gv = c.tensor_export_sorted(0, len(vals))
+    assert np.array_equal(gs, ss) and np.array_equal(gv, sv)
+    c.sample("stratified", 500, 700, 3001)
+    for stratum, n in ((0, 500), (1, 700)):
+        g_s, g_j, _, g_a = c.sample_export(stratum, 0, n)
+        o_s, o_j, _, o_a = orc.sample_export(t, stratum, 3001, 0, 0, n, 0, n)
+        assert np.array_equal(g_s, o_s) and np.array_equal(g_j, o_j) and np.array_equal(g_a, o_a)
+    A = _model(c, len(dims))
+    c.loss_grad("gaussian")
+    G = [c.grad_get(k) for k in range(len(dims))]
+    Go, S, _ = orc.sampled_grad(t, A, "gaussian", 3001, 0, 0, 500, 700)
+    _grad_check(G, Go, S, TOL["fp64"], f"d={len(dims)}")
