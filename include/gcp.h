@@ -162,7 +162,8 @@ gcp_status gcp_dist_set_async(gcp_ctx* ctx, int64_t tau, const gcp_adam_params* 
  * the nonzeros lexicographically (i_1 most significant, reading R15), rejects
  * duplicates, and builds the hash set of block-linearised keys (u64, or u128
  * when the block has >= 2^64 entries).  Replaces any previous tensor and drops
- * the model.  Blocks; collective for nranks > 1 (global N and M checks). */
+ * the model (both freed before the ingest; on failure the context has no
+ * tensor).  Blocks; collective for nranks > 1 (global N and M checks). */
 gcp_status gcp_tensor_create(gcp_ctx* ctx, int d, const int64_t* dims, int64_t nnz,
                              const int64_t* subs, const double* vals);
 

@@ -371,6 +371,10 @@ void gcp_destroy(gcp_ctx* c) {
     for (int k = 0; k < kMaxModes; ++k)
         if (c->slice[k]) ncclCommDestroy(c->slice[k]);
     twosided_free(c);
+    if (c->scratch_pool) {
+        cudaStreamSynchronize(c->stream);
+        cudaMemPoolDestroy(c->scratch_pool);
+    }
     if (c->devcomm_ready) ncclDevCommDestroy(c->world, &c->devcomm);
     if (c->world) ncclCommDestroy(c->world);
     delete c;
@@ -443,12 +447,26 @@ gcp_status gcp_tensor_create(gcp_ctx* c, int d, const int64_t* dims, int64_t nnz
             g->M *= (unsigned __int128)(g->hi[k] - g->lo[k]);
         }
     }
+    // Replace: drop the previous model and tensor before the ingest, so its
+    // scratch reuses their memory (the pool keeps it mapped) instead of growing
+    // past them.  A failed ingest leaves the context without a tensor.
+    free_model(c);
+    gfree(c, c->d_rec);
+    gfree(c, c->d_hash);
+    gfree(c, c->d_keys);
+    gfree(c, c->d_filter);
+    c->d_rec = nullptr;
+    c->d_hash = nullptr;
+    c->d_keys = nullptr;
+    c->d_filter = nullptr;
+    c->filter_sectors = 0;
+    c->have_tensor = false;
+    c->bound = false;
     gcp_status st = ingest(c, g, nnz, subs, vals);
     if (st != GCP_OK) {
         delete g;
         return st;
     }
-    free_model(c);
     c->d = d;
     for (int k = 0; k < kMaxModes; ++k) {
         c->dims[k] = k < d ? g->dims[k] : 0;
@@ -660,26 +678,13 @@ gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* la
     if (k < 0 || k >= c->d) return set_error(GCP_E_RANGE, "gcp_model_set: mode out of range");
     if (!rows) return set_error(GCP_E_ARG, "gcp_model_set: rows NULL");
     const int64_t b = c->hi[k] - c->lo[k];
-    const size_t n = (size_t)b * c->R_pad;
-    if (c->prec == GCP_FP32) {
-        std::vector<float> h(n, 0.f);
-        for (int64_t i = 0; i < b; ++i)
-            for (int r = 0; r < c->R; ++r) h[(size_t)i * c->R_pad + r] = (float)rows[i * c->R + r];
-        CUDA_TRY(c, cudaMemcpy2DAsync((float*)c->d_A + phys_off(c, k), (size_t)c->ag_stride * 4, h.data(),
-                                      (size_t)c->R_pad * 4, (size_t)c->R_pad * 4, (size_t)b, cudaMemcpyHostToDevice,
-                                      c->stream),
-                 "model_set");
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
-    } else {
-        std::vector<double> h(n, 0.0);
-        for (int64_t i = 0; i < b; ++i)
-            for (int r = 0; r < c->R; ++r) h[(size_t)i * c->R_pad + r] = rows[i * c->R + r];
-        CUDA_TRY(c, cudaMemcpy2DAsync((double*)c->d_A + phys_off(c, k), (size_t)c->ag_stride * 8, h.data(),
-                                      (size_t)c->R_pad * 8, (size_t)c->R_pad * 8, (size_t)b, cudaMemcpyHostToDevice,
-                                      c->stream),
-                 "model_set");
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
-    }
+    // H2D of the packed fp64 rows, then widen / narrow and pad on the device
+    double* d_rows = nullptr;
+    CUDA_TRY(c, gmalloc(c, &d_rows, (size_t)std::max<int64_t>(b, 1) * c->R * 8), "model_set");
+    CUDA_TRY(c, cudaMemcpyAsync(d_rows, rows, (size_t)b * c->R * 8, cudaMemcpyHostToDevice, c->stream), "model_set");
+    CUDA_TRY(c, launch_rows_in(c, d_rows, (char*)c->d_A + (size_t)phys_off(c, k) * tsz(c), b), "model_set");
+    gfree(c, d_rows);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
     if (lambda) {
         std::vector<double> l64(c->R_pad, 0.0);
         std::vector<float> l32(c->R_pad, 0.f);
@@ -695,30 +700,16 @@ gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* la
     return server_reset(c);   // FedAdam: the server copy starts from the model as set
 }
 
-// rows of A or G (row stride ag_stride) of mode k's block to a packed R_pad-wide host copy
+// rows of A or G (row stride ag_stride) of mode k's block as packed fp64 rows (b x R) in host memory
 static gcp_status read_rows(gcp_ctx* c, const void* base, int k, double* out, const char* what) {
     const int64_t b = c->hi[k] - c->lo[k];
-    const size_t n = (size_t)b * c->R_pad;
-    const size_t ts = tsz(c);
-    if (c->prec == GCP_FP32) {
-        std::vector<float> h(n);
-        CUDA_TRY(c, cudaMemcpy2DAsync(h.data(), (size_t)c->R_pad * ts, (const float*)base + phys_off(c, k),
-                                      (size_t)c->ag_stride * ts, (size_t)c->R_pad * ts, (size_t)b,
-                                      cudaMemcpyDeviceToHost, c->stream),
-                 what);
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
-        for (int64_t i = 0; i < b; ++i)
-            for (int r = 0; r < c->R; ++r) out[i * c->R + r] = h[(size_t)i * c->R_pad + r];
-    } else {
-        std::vector<double> h(n);
-        CUDA_TRY(c, cudaMemcpy2DAsync(h.data(), (size_t)c->R_pad * ts, (const double*)base + phys_off(c, k),
-                                      (size_t)c->ag_stride * ts, (size_t)c->R_pad * ts, (size_t)b,
-                                      cudaMemcpyDeviceToHost, c->stream),
-                 what);
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
-        for (int64_t i = 0; i < b; ++i)
-            for (int r = 0; r < c->R; ++r) out[i * c->R + r] = h[(size_t)i * c->R_pad + r];
-    }
+    // pack and widen to fp64 on the device, then one contiguous D2H into the caller's rows
+    double* d_rows = nullptr;
+    CUDA_TRY(c, gmalloc(c, &d_rows, (size_t)std::max<int64_t>(b, 1) * c->R * 8), what);
+    CUDA_TRY(c, launch_rows_out(c, (const char*)base + (size_t)phys_off(c, k) * tsz(c), d_rows, b), what);
+    CUDA_TRY(c, cudaMemcpyAsync(out, d_rows, (size_t)b * c->R * 8, cudaMemcpyDeviceToHost, c->stream), what);
+    gfree(c, d_rows);
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), what);
     return GCP_OK;
 }
 

@@ -132,6 +132,7 @@ struct gcp_ctx {
     gcp_membership member = GCP_MEMBER_HASH;   // zero-test structure built at ingest
     uint64_t* d_keys = nullptr;                // sorted keys (GCP_MEMBER_SORTED)
     uint64_t* d_filter = nullptr;              // L2-resident negative test in front of the zero test
+    cudaMemPool_t scratch_pool = nullptr;      // ingest scratch (ingest.cu)
     uint64_t filter_sectors = 0;
     // ---- model
     bool have_model = false;
@@ -220,6 +221,8 @@ cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* 
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
 cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);
+cudaError_t launch_rows_in(gcp_ctx* c, const double* src, void* dst, int64_t b);    // packed rows -> layout
+cudaError_t launch_rows_out(gcp_ctx* c, const void* src, double* dst, int64_t b);   // layout -> packed rows
 int sample_kernel_blocks(gcp_ctx* c);
 
 // ingest.cu
@@ -255,7 +258,15 @@ namespace gcp {
 // cudaMalloc / cudaFree page mapping every time.
 template <typename P>
 inline cudaError_t gmalloc(gcp_ctx* c, P** p, size_t bytes) {
-    return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, c->stream);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes, c->stream);
+    if (e == cudaErrorMemoryAllocation && c->scratch_pool) {
+        // the ingest scratch pool keeps its memory mapped between ingests: give it back and retry
+        cudaGetLastError();
+        cudaStreamSynchronize(c->stream);
+        cudaMemPoolTrimTo(c->scratch_pool, 0);
+        e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes, c->stream);
+    }
+    return e;
 }
 inline cudaError_t gfree(gcp_ctx* c, void* p) { return p ? cudaFreeAsync(p, c->stream) : cudaSuccess; }
 }  // namespace gcp

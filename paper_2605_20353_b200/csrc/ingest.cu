@@ -10,6 +10,9 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -220,6 +223,43 @@ cudaError_t launch_contains(gcp_ctx* c, int64_t n, const int64_t* coords, int8_t
         if (e_ != cudaSuccess) { err = e_; goto cleanup; } \
     } while (0)
 
+// Ingest scratch (staging, keys, permutations, sort temp) comes from a pool of
+// its own: repeated ingests of similar size find their blocks again instead of
+// fragmenting the default pool that holds the tensor and the model (which made
+// every few ingests map fresh memory).  Trimmed after an ingest when the
+// device is short of free memory, and by gmalloc when an allocation fails.
+static cudaError_t scratch_pool(gcp_ctx* c) {
+    if (c->scratch_pool) return cudaSuccess;
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = c->dev;
+    cudaError_t e = cudaMemPoolCreate(&c->scratch_pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;
+    return cudaMemPoolSetAttribute(c->scratch_pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+template <typename P>
+static cudaError_t smalloc(gcp_ctx* c, P** p, size_t bytes) {
+    cudaError_t e = scratch_pool(c);
+    if (e != cudaSuccess) return e;
+    return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, c->scratch_pool, c->stream);
+}
+static void sfree(gcp_ctx* c, void* p) {
+    if (p) cudaFreeAsync(p, c->stream);
+}
+static void scratch_trim_if_tight(gcp_ctx* c) {
+    size_t fr = 0, tot = 0;
+    if (!c->scratch_pool || cudaMemGetInfo(&fr, &tot) != cudaSuccess) return;
+    // keep the scratch mapped for the next ingest unless the device is short of
+    // memory (gmalloc also trims it and retries when a later allocation fails)
+    if (fr < tot / 8) {
+        cudaStreamSynchronize(c->stream);
+        cudaMemPoolTrimTo(c->scratch_pool, 0);
+    }
+}
+
 template <typename T, typename PermT>
 static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h,
                               const double* vals_h) {
@@ -257,18 +297,30 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
     uint64_t* new_keys = nullptr;
     uint64_t* new_filter = nullptr;
     const uint64_t fsect = filter_sectors_for(c, nnz, sorted_member ? 4 : 12);
+    // diagnostics: GCP_INGEST_TRACE=1 syncs after each phase and prints its time
+    const char* trace_env = getenv("GCP_INGEST_TRACE");
+    const bool trace = trace_env && trace_env[0] == '1';
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[gcp ingest] %-28s %9.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
 
-    CK(gmalloc(c, &d_flags, sizeof(unsigned)));
+    CK(smalloc(c, &d_flags, sizeof(unsigned)));
     CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
     if (nnz > 0) {
         // 1) stream the host COO through the staging buffer, converting on the fly
-        CK(gmalloc(c, &coords, (size_t)nnz * d * 4));
-        CK(gmalloc(c, &valt, (size_t)nnz * sizeof(T)));
-        CK(gmalloc(c, &k0, (size_t)nnz * 8));
-        if (k128) CK(gmalloc(c, &h0, (size_t)nnz * 8));
-        CK(gmalloc(c, &p0, (size_t)nnz * sizeof(PermT)));
-        CK(gmalloc(c, &d_sc, (size_t)chunk * d * 8));
-        CK(gmalloc(c, &d_vc, (size_t)chunk * 8));
+        CK(smalloc(c, &coords, (size_t)nnz * d * 4));
+        CK(smalloc(c, &valt, (size_t)nnz * sizeof(T)));
+        CK(smalloc(c, &k0, (size_t)nnz * 8));
+        if (k128) CK(smalloc(c, &h0, (size_t)nnz * 8));
+        CK(smalloc(c, &p0, (size_t)nnz * sizeof(PermT)));
+        CK(smalloc(c, &d_sc, (size_t)chunk * d * 8));
+        CK(smalloc(c, &d_vc, (size_t)chunk * 8));
         for (int64_t b = 0; b < nnz; b += chunk) {
             const int64_t n = std::min(chunk, nnz - b);
             CK(cudaMemcpyAsync(d_sc, subs_h + b * d, (size_t)n * d * 8, cudaMemcpyDefault, st));
@@ -279,19 +331,20 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
         }
         CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        gfree(c, d_sc); d_sc = nullptr;
-        gfree(c, d_vc); d_vc = nullptr;
+        mark("H2D + convert");
+        sfree(c, d_sc); d_sc = nullptr;
+        sfree(c, d_vc); d_vc = nullptr;
         if (flags & BAD_RANGE) { status = set_error(GCP_E_RANGE, "gcp_tensor_create: coordinate outside dims / block"); goto cleanup; }
         if (flags & BAD_VALUE) { status = set_error(GCP_E_ARG, "gcp_tensor_create: non-finite value"); goto cleanup; }
         // 2) LSD radix sort of (key, perm): low word, then stably the high word
-        CK(gmalloc(c, &k1, (size_t)nnz * 8));
-        CK(gmalloc(c, &p1, (size_t)nnz * sizeof(PermT)));
+        CK(smalloc(c, &k1, (size_t)nnz * 8));
+        CK(smalloc(c, &p1, (size_t)nnz * sizeof(PermT)));
         {
             cub::DoubleBuffer<uint64_t> keys(k0, k1);
             cub::DoubleBuffer<PermT> pm(p0, p1);
             const int lo_bits = k128 ? 64 : std::max(kbits, 1);
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, pm, nnz, 0, lo_bits, st));
-            CK(gmalloc(c, &tmp, tmp_bytes));
+            CK(smalloc(c, &tmp, tmp_bytes));
             CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, pm, nnz, 0, lo_bits, st));
             if (k128) {
                 // high words in the current order, then a stable sort on them
@@ -303,9 +356,9 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
                 size_t tb2 = 0;
                 CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hk, pm, nnz, 0, kbits - 64, st));
                 if (tb2 > tmp_bytes) {
-                    gfree(c, tmp);
+                    sfree(c, tmp);
                     tmp = nullptr;
-                    CK(gmalloc(c, &tmp, tb2));
+                    CK(smalloc(c, &tmp, tb2));
                     tmp_bytes = tb2;
                 }
                 CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, hk, pm, nnz, 0, kbits - 64, st));
@@ -319,9 +372,10 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
             CK(cudaGetLastError());
             c->launches++;
         }
-        gfree(c, tmp); tmp = nullptr;
-        gfree(c, k1); k1 = nullptr;
-        gfree(c, perm == p0 ? p1 : p0);
+        mark("radix sort + sorted keys");
+        sfree(c, tmp); tmp = nullptr;
+        sfree(c, k1); k1 = nullptr;
+        sfree(c, perm == p0 ? p1 : p0);
         if (perm == p0) p1 = nullptr; else p0 = nullptr;
         // 3) duplicates, records
         k_dupcheck<<<nb, 256, 0, st>>>(nnz, skl, skh, d_flags);
@@ -334,13 +388,14 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
         CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (flags & BAD_DUP) { status = set_error(GCP_E_DUP, "gcp_tensor_create: duplicate coordinates"); goto cleanup; }
-        gfree(c, coords); coords = nullptr;
-        gfree(c, valt); valt = nullptr;
-        gfree(c, p0); p0 = nullptr;
-        gfree(c, p1); p1 = nullptr;
+        sfree(c, coords); coords = nullptr;
+        sfree(c, valt); valt = nullptr;
+        sfree(c, p0); p0 = nullptr;
+        sfree(c, p1); p1 = nullptr;
     } else {
         CK(gmalloc(c, &new_rec, (size_t)rec_words * 4));
     }
+    mark("dup check + records");
     // 4) zero-test structure
     CK(gmalloc(c, &new_hash, (size_t)slots * 8 * kw));
     CK(cudaMemsetAsync(new_hash, 0xFF, (size_t)slots * 8 * kw, st));
@@ -359,10 +414,11 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
         }
     }
     CK(cudaStreamSynchronize(st));
+    mark("hash / keys / filter");
 
 cleanup:
-    gfree(c, d_flags); gfree(c, d_sc); gfree(c, d_vc); gfree(c, coords); gfree(c, valt);
-    gfree(c, k0); gfree(c, k1); gfree(c, h0); gfree(c, h1); gfree(c, p0); gfree(c, p1); gfree(c, tmp);
+    sfree(c, d_flags); sfree(c, d_sc); sfree(c, d_vc); sfree(c, coords); sfree(c, valt);
+    sfree(c, k0); sfree(c, k1); sfree(c, h0); sfree(c, h1); sfree(c, p0); sfree(c, p1); sfree(c, tmp);
     if (err != cudaSuccess || status != GCP_OK) {
         gfree(c, new_rec);
         gfree(c, new_hash);
@@ -394,11 +450,15 @@ cleanup:
 
 gcp_status ingest(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h, const double* vals_h) {
     const bool p32 = nnz < ((int64_t)1 << 32);
+    gcp_status st;
     if (c->prec == GCP_FP32)
-        return p32 ? ingest_impl<float, uint32_t>(c, g, nnz, subs_h, vals_h)
-                   : ingest_impl<float, uint64_t>(c, g, nnz, subs_h, vals_h);
-    return p32 ? ingest_impl<double, uint32_t>(c, g, nnz, subs_h, vals_h)
-               : ingest_impl<double, uint64_t>(c, g, nnz, subs_h, vals_h);
+        st = p32 ? ingest_impl<float, uint32_t>(c, g, nnz, subs_h, vals_h)
+                 : ingest_impl<float, uint64_t>(c, g, nnz, subs_h, vals_h);
+    else
+        st = p32 ? ingest_impl<double, uint32_t>(c, g, nnz, subs_h, vals_h)
+                 : ingest_impl<double, uint64_t>(c, g, nnz, subs_h, vals_h);
+    scratch_trim_if_tight(c);
+    return st;
 }
 
 }  // namespace gcp

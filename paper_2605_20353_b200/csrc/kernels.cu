@@ -108,6 +108,49 @@ cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s) {
     return cudaGetLastError();
 }
 
+// packed host-order rows (b x R doubles) <-> the factor layout (rows of R_pad T
+// at row stride `stride`, zero padding): model_set / model_get on the device
+template <typename T>
+__global__ void k_rows_in(const double* __restrict__ src, T* __restrict__ dst, int64_t b, int R, int R_pad,
+                          int stride) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < b * R_pad;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / R_pad;
+        const int r = (int)(x % R_pad);
+        dst[i * stride + r] = r < R ? (T)src[i * R + r] : T(0);
+    }
+}
+template <typename T>
+__global__ void k_rows_out(const T* __restrict__ src, double* __restrict__ dst, int64_t b, int R, int stride) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < b * R;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / R;
+        dst[x] = (double)src[i * stride + (int)(x % R)];
+    }
+}
+
+cudaError_t launch_rows_in(gcp_ctx* c, const double* src, void* dst, int64_t b) {
+    if (b == 0) return cudaSuccess;
+    const int64_t n = b * c->R_pad;
+    if (c->prec == GCP_FP32)
+        k_rows_in<float><<<grid_for(c, n), 256, 0, c->stream>>>(src, (float*)dst, b, c->R, c->R_pad, c->ag_stride);
+    else
+        k_rows_in<double><<<grid_for(c, n), 256, 0, c->stream>>>(src, (double*)dst, b, c->R, c->R_pad, c->ag_stride);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_out(gcp_ctx* c, const void* src, double* dst, int64_t b) {
+    if (b == 0) return cudaSuccess;
+    const int64_t n = b * c->R;
+    if (c->prec == GCP_FP32)
+        k_rows_out<float><<<grid_for(c, n), 256, 0, c->stream>>>((const float*)src, dst, b, c->R, c->ag_stride);
+    else
+        k_rows_out<double><<<grid_for(c, n), 256, 0, c->stream>>>((const double*)src, dst, b, c->R, c->ag_stride);
+    c->launches++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n) {
     if (n == 0) return cudaSuccess;
     if (c->prec == GCP_FP32)

@@ -203,6 +203,12 @@ def test_zero_gradient_and_errors(gcp):
     with pytest.raises(gcp.GcpError) as e:
         c.loss_grad("poisson")
     assert e.value.name == "GCP_E_STATE"
+    # a failed replacement leaves the context without a tensor (the old one is freed first)
+    with pytest.raises(gcp.GcpError):
+        c.tensor_create(dims, np.array([[0, 0, 0], [0, 0, 0]]), np.array([1.0, 2.0]))
+    with pytest.raises(gcp.GcpError) as e:
+        c.sample("stratified", 10, 10, 1)
+    assert e.value.name == "GCP_E_STATE"
     # one zero in 10^4 entries: the rejection cap fires (reading R5) and is sticky
     dims = (10, 10, 100)
     lin = np.arange(10 * 10 * 100)[1:]
