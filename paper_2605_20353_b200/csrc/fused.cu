@@ -343,10 +343,10 @@ static void fused_trace_collect(gcp_ctx* c) {
         cudaStreamSynchronize(c->stream) != cudaSuccess)
         return;
     unsigned long long t0 = ~0ull;
-    for (int b = 0; b < c->fused_ctas; ++b) t0 = std::min(t0, h[(size_t)b * kTraceStamps]);
+    for (int b = 0; b < c->fused_grid; ++b) t0 = std::min(t0, h[(size_t)b * kTraceStamps]);
     for (int i = 1; i < kTraceStamps; ++i) {
         unsigned long long mx = 0;
-        for (int b = 0; b < c->fused_ctas; ++b) mx = std::max(mx, h[(size_t)b * kTraceStamps + i]);
+        for (int b = 0; b < c->fused_grid; ++b) mx = std::max(mx, h[(size_t)b * kTraceStamps + i]);
         c->ftrace_acc[i] += mx > t0 ? (double)(mx - t0) * 1e-3 : 0.0;
     }
     c->ftrace_n += 1;
@@ -381,6 +381,14 @@ gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower) {
     }
     fa.vec_begin[c->d] = acc;
     fa.zero_vecs = c->n_coef / VE;
+    // grid: one CTA per SM.  Fewer CTAs for the small c2 exchange (32-64 of
+    // 148) measured within run-to-run noise (profiles/fused_grid_r01.sh).
+    // Must be identical on every rank: the barrier pairs CTA i across ranks.
+    // GCP_FUSED_GRID overrides (experiments).
+    int grid = c->fused_ctas;
+    const char* genv = getenv("GCP_FUSED_GRID");
+    if (genv && atoi(genv) > 0) grid = std::min(c->fused_ctas, atoi(genv));
+    c->fused_grid = grid;
     fa.trace = nullptr;
     if (!c->capturing && fused_trace_on()) {
         if (!c->ftrace) {
@@ -397,12 +405,12 @@ gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower) {
     cudaEvent_t ev;
     prof_begin(c, PROF_COMM, &ev);
     if (c->prec == GCP_FP32)
-        k_fused_exchange<float><<<c->fused_ctas, 256, 0, c->stream>>>(
+        k_fused_exchange<float><<<grid, 256, 0, c->stream>>>(
             c->devcomm, c->winA, c->winG[cur], (float*)gnext, (float*)c->d_B, (float*)c->d_C, fa, (float)p->rate,
             (float)p->beta1, (float)p->beta2, (float)p->eps, (float)bc1, (float)bc2, (float)lower,
             c->capturing ? c->d_step : nullptr, (long long)(c->t - c->graph_t0));
     else
-        k_fused_exchange<double><<<c->fused_ctas, 256, 0, c->stream>>>(
+        k_fused_exchange<double><<<grid, 256, 0, c->stream>>>(
             c->devcomm, c->winA, c->winG[cur], (double*)gnext, (double*)c->d_B, (double*)c->d_C, fa, p->rate,
             p->beta1, p->beta2, p->eps, bc1, bc2, lower, c->capturing ? c->d_step : nullptr,
             (long long)(c->t - c->graph_t0));

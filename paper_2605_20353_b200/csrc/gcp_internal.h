@@ -105,7 +105,8 @@ struct gcp_ctx {
     // fused NVLink exchange (fused.cu): symmetric windows + device communicator
     bool fused = false, devcomm_ready = false;
     bool multimem = false;                        // NVLS multicast usable on the LSA team
-    int fused_ctas = 0;                           // grid of the fused exchange (one LSA barrier each)
+    int fused_ctas = 0;                           // max grid of the fused exchange (one LSA barrier each)
+    int fused_grid = 0;                           // grid of the last launch
     void* ftrace = nullptr;                       // GCP_FUSED_TRACE diagnostics
     double ftrace_acc[16] = {0};
     int64_t ftrace_n = 0;
