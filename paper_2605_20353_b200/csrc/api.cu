@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gcp_internal.h"
 
 using namespace gcp;
@@ -302,6 +304,12 @@ bool valid_loss(int loss) { return loss >= 0 && loss <= 2; }
 
 }  // namespace
 
+// NVTX ranges around the ABI's phases (no-ops unless a profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // ================================================================ ABI
 extern "C" {
 
@@ -403,6 +411,7 @@ gcp_status gcp_set_membership(gcp_ctx* c, gcp_membership m) {
 gcp_status gcp_tensor_create(gcp_ctx* c, int d, const int64_t* dims, int64_t nnz, const int64_t* subs,
                              const double* vals) {
     ENTER(c);
+    NvtxRange nvtx_("gcp_tensor_create");
     if (d < 2 || d > kMaxD) return set_error(GCP_E_ARG, "gcp_tensor_create: need 2 <= d <= 6");
     if (!dims || nnz < 0 || (nnz > 0 && (!subs || !vals)))
         return set_error(GCP_E_ARG, "gcp_tensor_create: bad pointers / nnz");
@@ -798,6 +807,7 @@ gcp_status gcp_sample_export(gcp_ctx* c, int stratum, int64_t first, int64_t cou
 
 gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     ENTER(c);
+    NvtxRange nvtx_("gcp_loss_grad");
     if (!c->have_model || !c->bound) return set_error(GCP_E_STATE, "gcp_loss_grad: need model and gcp_sample");
     if (!valid_loss(loss)) return set_error(GCP_E_ARG, "gcp_loss_grad: bad loss");
     // async schemes: averaging / server step before this iteration's sampling (Alg. 3-4)
@@ -833,6 +843,7 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
 
 gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     ENTER(c);
+    NvtxRange nvtx_("gcp_adam_step");
     if (!p) return set_error(GCP_E_ARG, "gcp_adam_step: NULL params");
     if (!c->have_grad) return set_error(GCP_E_STATE, "gcp_adam_step: no gradient (call gcp_loss_grad)");
     if (!(p->beta1 >= 0 && p->beta1 < 1 && p->beta2 >= 0 && p->beta2 < 1 && p->eps > 0 && p->rate >= 0))
@@ -893,6 +904,7 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
 
 gcp_status gcp_loss_estimate(gcp_ctx* c, gcp_loss loss, int64_t f_nz, int64_t f_z, uint64_t seed, double* out) {
     ENTER(c);
+    NvtxRange nvtx_("gcp_loss_estimate");
     if (!c->have_model) return set_error(GCP_E_STATE, "gcp_loss_estimate: no model");
     if (!valid_loss(loss)) return set_error(GCP_E_ARG, "gcp_loss_estimate: bad loss");
     if (!out || f_nz < 0 || f_z < 0 || f_nz + f_z == 0) return set_error(GCP_E_ARG, "gcp_loss_estimate: args");
@@ -912,6 +924,7 @@ gcp_status gcp_loss_estimate(gcp_ctx* c, gcp_loss loss, int64_t f_nz, int64_t f_
 
 gcp_status gcp_fit_begin(gcp_ctx* c, const gcp_fit_params* p, double* initial_est) {
     ENTER(c);
+    NvtxRange nvtx_("gcp_fit_begin");
     if (!p) return set_error(GCP_E_ARG, "gcp_fit_begin: NULL params");
     if (!c->have_model) return set_error(GCP_E_STATE, "gcp_fit_begin: no model");
     if (p->epochs < 0 || p->iters_per_epoch < 1 || p->max_fails < 1 || !(p->decay >= 0) || !valid_loss(p->loss))
@@ -1025,6 +1038,7 @@ static gcp_status epoch_graph(gcp_ctx* c, gcp_loss loss, const gcp_adam_params& 
 
 gcp_status gcp_fit_epoch(gcp_ctx* c, double* est_out, int* accepted_out, int* done_out) {
     ENTER(c);
+    NvtxRange nvtx_("gcp_fit_epoch");
     if (!c->fit_active) return set_error(GCP_E_STATE, "gcp_fit_epoch: call gcp_fit_begin first");
     const gcp_fit_params& p = c->fp;
     if (c->epoch >= p.epochs || c->fails >= p.max_fails) {

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--l2fetch", default="", help="comma list of cudaLimitMaxL2FetchGranularity values to sweep")
     ap.add_argument("--strategies", default="stratified", help="comma list: stratified,semi")
     ap.add_argument("--membership", default="hash", help="hash or sorted (row f4)")
+    ap.add_argument("--p", type=int, default=-1, help="nonzero samples per iteration (default: the config's)")
+    ap.add_argument("--q", type=int, default=-1, help="zero samples per iteration (default: the config's)")
     args = ap.parse_args()
     import paper_2605_20353_b200 as g
     c = gcp_synth.CONFIGS[args.config]
@@ -46,14 +48,16 @@ def main():
     ctx.tensor_create_ptr(c["dims"], vals_h.numel(), subs_h.data_ptr(), vals_h.data_ptr())
     t_ingest = time.time() - t0
     ctx.model_init(c["R"], s["model"])
-    ctx.sample("stratified", c["s"], c["s"], s["sample"])
+    P = c["s"] if args.p < 0 else args.p
+    Q = c["s"] if args.q < 0 else args.q
+    ctx.sample("stratified", P, Q, s["sample"])
     for _ in range(3):
         ctx.loss_grad(c["loss"])
         ctx.adam_step()
     ctx.loss_estimate(c["loss"], c["f"], c["f"], 2)
     sweep = [int(x) for x in args.l2fetch.split(",")] if args.l2fetch else [None]
     for strat, l2f in [(st, l) for st in args.strategies.split(",") for l in sweep]:
-        ctx.sample(strat, c["s"], c["s"], s["sample"])
+        ctx.sample(strat, P, Q, s["sample"])
         if l2f is not None:   # device-wide hint through the process's CUDA runtime
             import ctypes
             rt = ctypes.CDLL("libcudart.so.12")
@@ -71,7 +75,8 @@ def main():
         for k in ("grad", "adam", "loss"):
             ms, n = ctx.profile_get(k)
             out[k + "_ms"] = ms / max(n, 1)
-        out["samples_per_s_k2"] = 2 * c["s"] / (out["grad_ms"] * 1e-3)
+        out["p"], out["q"] = P, Q
+        out["samples_per_s_k2"] = (P + Q) / (out["grad_ms"] * 1e-3)
         print(json.dumps(out), flush=True)
 
 
