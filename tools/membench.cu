@@ -167,6 +167,35 @@ __global__ void k2_skeleton_dram(const uint4* __restrict__ big, uint64_t nbig, f
     if (acc == 1.2345f) *sink = acc;
 }
 
+// random 16-B loads with an explicit L2 prefetch-size qualifier (PF: 0 none, 64, 128, 256)
+template <int PF>
+__global__ void rand_load_pf(const uint4* __restrict__ a, uint64_t n, int64_t total, uint32_t* sink) {
+    uint32_t acc = 0;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < total; i += nt * 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4* p = a + __umul64hi(mix(i + k * nt), n);
+            if constexpr (PF == 64)
+                asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "l"(p));
+            else if constexpr (PF == 128)
+                asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "l"(p));
+            else if constexpr (PF == 1)
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "l"(p));
+            else
+                v[k] = __ldg(p);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc += v[k].x ^ v[k].w;
+    }
+    if (acc == 0x12345678u) *sink = acc;
+}
+
 __global__ void copy4(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = a[i];
@@ -228,6 +257,16 @@ int main() {
             float ms = timeit([&] { smem_red<<<sms * bps, 256, sb>>>((float*)sink, srows, total); });
             printf("\"smem_red64_rows%d_b%d\": %.3e, ", srows, bps, total / (ms * 1e-3));
         }
+    }
+    for (int blocks : {sms * 4, sms * 16}) {
+        float ms = timeit([&] { rand_load_pf<0><<<blocks, 256>>>(A, big / 16, total, sink); });
+        printf("\"rand16_pf0_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_load_pf<1><<<blocks, 256>>>(A, big / 16, total, sink); });
+        printf("\"rand16_noalloc_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_load_pf<64><<<blocks, 256>>>(A, big / 16, total, sink); });
+        printf("\"rand16_pf64_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+        ms = timeit([&] { rand_load_pf<128><<<blocks, 256>>>(A, big / 16, total, sink); });
+        printf("\"rand16_pf128_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
     }
     // K2 skeleton on c2's shape: 30,000 rows of 64 B per array (A and G 1.9 MB), 2e7 samples
     {
