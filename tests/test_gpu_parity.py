@@ -288,13 +288,15 @@ def test_sorted_membership_same_draws(gcp, orc, shape):
     _grad_check(G, Go, S, 1e-4, "sorted membership")
 
 
-@pytest.mark.parametrize("graphs", ["1", "0"])
-def test_fit_matches_oracle(gcp, orc, graphs, monkeypatch):
+@pytest.mark.parametrize("graphs,interleave", [("1", "0"), ("0", "0"), ("1", "1")])
+def test_fit_matches_oracle(gcp, orc, graphs, interleave, monkeypatch):
     """The epoch loop (annealing, R20) against oracle.fit, fp64, on a side
     stream: with GCP_GRAPHS=1 each epoch's iterations replay as one CUDA graph
-    with the step state on the device; with 0 they launch one by one."""
+    with the step state on the device; with 0 they launch one by one; and the
+    graph path with A/G rows interleaved (the layout c4 uses)."""
     import torch
     monkeypatch.setenv("GCP_GRAPHS", graphs)
+    monkeypatch.setenv("GCP_AG_INTERLEAVE", interleave)
     dims = (20, 30, 40)
     subs, vals = _tensor("poisson")
     stream = torch.cuda.Stream(0)
