@@ -196,6 +196,33 @@ __global__ void rand_load_pf(const uint4* __restrict__ a, uint64_t n, int64_t to
     if (acc == 0x12345678u) *sink = acc;
 }
 
+// TMA bulk reduction alternative to red.add.v4: each warp stages 8 rows of 64 B
+// in shared memory and 8 lanes issue one cp.reduce.async.bulk (.add.f32) each
+// into random rows of an L2-resident array (double-buffered per warp).
+__global__ void bulk_red(float* G, uint64_t rows, int64_t total_rows) {
+    __shared__ __align__(128) float4 buf[8][2][32];   // [warp][stage][lane]: 8 rows x 64 B
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int stage = 0;
+    for (int64_t i = gw * 8; i < total_rows; i += nw * 8) {
+        if (lane < 8) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        buf[w][stage][lane] = make_float4(1.f, 1.f, 1.f, 1.f);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane < 8) {
+            const uint64_t r = __umul64hi(mix(i + lane), rows);
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[w][stage][lane * 4]);
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 64;"
+                         :: "l"(G + r * 16), "r"(sa) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        stage ^= 1;
+    }
+    if (lane < 8) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void copy4(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = a[i];
@@ -267,6 +294,10 @@ int main() {
         printf("\"rand16_pf64_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
         ms = timeit([&] { rand_load_pf<128><<<blocks, 256>>>(A, big / 16, total, sink); });
         printf("\"rand16_pf128_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
+    }
+    for (int blocks : {sms * 2, sms * 4, sms * 8}) {
+        float ms = timeit([&] { bulk_red<<<blocks, 256>>>((float*)S, small / 64, total); });
+        printf("\"bulkred64_l2_rows_b%d\": %.3e, ", blocks, total / (ms * 1e-3));
     }
     // K2 skeleton on c2's shape: 30,000 rows of 64 B per array (A and G 1.9 MB), 2e7 samples
     {
