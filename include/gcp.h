@@ -12,7 +12,10 @@
  *  - Returns gcp_status; no C++ exception crosses the ABI.  On error
  *    gcp_last_error() returns a thread-local message.
  *  - Argument errors (GCP_E_ARG / GCP_E_RANGE / GCP_E_DUP / GCP_E_NO_*) are
- *    detected before any state changes (no partial mutation).
+ *    detected before any state changes (no partial mutation) -- except the
+ *    data errors gcp_tensor_create finds while ingesting (duplicates,
+ *    out-of-block coordinates, non-finite values), which leave the context
+ *    without a tensor (the previous one is freed first).
  *  - CUDA and NCCL failures, and a zero sample hitting the rejection cap, are
  *    sticky: the context enters an error state and every later call returns
  *    GCP_E_STATE (gcp_destroy still works).  A rejection-cap or CUDA fault in
@@ -260,7 +263,10 @@ gcp_status gcp_loss_estimate(gcp_ctx* ctx, gcp_loss loss, int64_t f_nz, int64_t 
  * epoch: iters_per_epoch x [gradient, exchange, Adam], then F^_e; accept
  * (checkpoint) if F^_e < best, else restore, rate *= decay, fails += 1;
  * *done_out = 1 when fails reached max_fails or the epoch budget is spent.
- * All three block; collective for nranks > 1. */
+ * On a non-legacy stream the epoch's iterations are captured once per
+ * schedule and replayed as one CUDA graph (not while profiling, for the
+ * two-sided layout or FedAdam; environment GCP_GRAPHS=0 disables it); results
+ * are the same either way.  All three block; collective for nranks > 1. */
 gcp_status gcp_fit_begin(gcp_ctx* ctx, const gcp_fit_params* p, double* initial_est);
 gcp_status gcp_fit_epoch(gcp_ctx* ctx, double* est_out, int* accepted_out, int* done_out);
 gcp_status gcp_fit(gcp_ctx* ctx, const gcp_fit_params* p, gcp_trace_fn trace, void* user,
