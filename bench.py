@@ -429,7 +429,9 @@ def main():
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": k2_avg_ms, "peak_source": peak_src,
                          "note": ("factors and G L2-resident: the algorithmic bytes are mostly served by L2, so "
                                   "frac > 1 is expected; see random_access_roofline and traffic (DRAM bytes)")
-                         if l2_ctx else "factors and G DRAM-resident: the honest HBM case"},
+                         if sum(w["dims"]) * w["R"] * 4 <= 32e6 else
+                         ("factors and G DRAM-resident: the honest HBM case; random_access_roofline is the "
+                          "measured ceiling of the same access pattern")},
             "random_access_roofline": l2_ctx,
             "clocks": clocks,
             "e2e": e2e,
