@@ -360,7 +360,9 @@ void gcp_destroy(gcp_ctx* c) {
     if (!c) return;
     DevGuard g(c->dev);
     cudaStreamSynchronize(c->stream);
+    c->closing = true;
     free_model(c);
+    fused_cache_release(c);
     gfree(c, c->d_rec);
     gfree(c, c->d_hash);
     gfree(c, c->d_keys);

@@ -31,6 +31,13 @@ static ncclDataType_t dtype(const gcp_ctx* c) { return c->prec == GCP_FP32 ? ncc
 static size_t tsz(const gcp_ctx* c) { return c->prec == GCP_FP32 ? 4 : 8; }
 
 gcp_status dist_make_slices(gcp_ctx* c) {
+    // the split depends only on the grid (every rank computes the same one), so a
+    // replace-ingest with the same grid keeps its communicators: ncclCommSplit is
+    // a collective costing ~0.1-1 s per mode
+    bool same = c->slice_d == c->d;
+    for (int k = 0; same && k < c->d; ++k) same = c->slice_grid[k] == c->grid[k] && c->slice[k] != nullptr;
+    if (same) return GCP_OK;
+    c->slice_d = 0;
     int b[kMaxModes];
     int rem = c->rank;
     for (int k = c->d - 1; k >= 0; --k) {
@@ -53,6 +60,8 @@ gcp_status dist_make_slices(gcp_ctx* c) {
         c->slice_size[k] = n;
         c->slice_rank[k] = r;
     }
+    for (int k = 0; k < c->d; ++k) c->slice_grid[k] = c->grid[k];
+    c->slice_d = c->d;
     return GCP_OK;
 }
 

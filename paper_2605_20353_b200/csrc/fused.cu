@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(256) k_fused_exchange(ncclDevComm comm, ncclWi
         if (r_ != ncclSuccess) return nccl_fail((c), r_, what);     \
     } while (0)
 
+static constexpr size_t kFusedCacheMax = (size_t)4 << 30;   // 4 GiB of kept windows at most
+
 static size_t round_win(size_t b) {
     const size_t g = (size_t)2 << 20;   // symmetric windows: whole 2-MB granules
     return (b + g - 1) / g * g;
@@ -271,10 +273,23 @@ gcp_status fused_alloc(gcp_ctx* c, size_t bytes) {
         c->devcomm_ready = true;
         c->multimem = reqs.lsaMultimem && c->devcomm.lsaMultimem.mcBasePtr != nullptr;
     }
-    for (int i = 0; i < 3; ++i) {
-        NCCL_TRY_F(c, ncclMemAlloc(bufs[i], wb), "ncclMemAlloc");
-        NCCL_TRY_F(c, ncclCommWindowRegister(c->world, *bufs[i], wb, wins[i], NCCL_WIN_COLL_SYMMETRIC),
-                   "ncclCommWindowRegister");
+    c->fwin_bytes = wb;
+    // every rank pads to the same window size, so all take the same branch here
+    if (c->fcache_bytes == wb) {
+        for (int i = 0; i < 3; ++i) {
+            *bufs[i] = c->fcache_buf[i];
+            *wins[i] = c->fcache_win[i];
+            c->fcache_buf[i] = nullptr;
+            c->fcache_win[i] = nullptr;
+        }
+        c->fcache_bytes = 0;
+    } else {
+        fused_cache_release(c);
+        for (int i = 0; i < 3; ++i) {
+            NCCL_TRY_F(c, ncclMemAlloc(bufs[i], wb), "ncclMemAlloc");
+            NCCL_TRY_F(c, ncclCommWindowRegister(c->world, *bufs[i], wb, wins[i], NCCL_WIN_COLL_SYMMETRIC),
+                       "ncclCommWindowRegister");
+        }
     }
     // slice members of every mode as LSA ranks, in world-rank order (== slice_rank order)
     int b[kMaxModes];
@@ -312,13 +327,34 @@ void fused_free(gcp_ctx* c) {
     void** bufs[3] = {&c->d_A, &c->d_G, &c->d_G2};
     ncclWindow_t* wins[3] = {&c->winA, &c->winG[0], &c->winG[1]};
     cudaStreamSynchronize(c->stream);
+    fused_cache_release(c);
+    // keep up to kFusedCacheMax of registered windows for the next model of the
+    // same size (replace-ingest jobs skip the collective deregister / register)
+    const size_t wb = c->fwin_bytes;
+    const bool keep = !c->closing && 3 * wb <= kFusedCacheMax && *wins[0] && *wins[1] && *wins[2];
     for (int i = 0; i < 3; ++i) {
-        if (*wins[i]) ncclCommWindowDeregister(c->world, *wins[i]);
-        if (*bufs[i]) ncclMemFree(*bufs[i]);
+        if (keep) {
+            c->fcache_buf[i] = *bufs[i];
+            c->fcache_win[i] = *wins[i];
+        } else {
+            if (*wins[i]) ncclCommWindowDeregister(c->world, *wins[i]);
+            if (*bufs[i]) ncclMemFree(*bufs[i]);
+        }
         *wins[i] = nullptr;
         *bufs[i] = nullptr;
     }
+    c->fcache_bytes = keep ? wb : 0;
     c->fused = false;
+}
+
+void fused_cache_release(gcp_ctx* c) {
+    for (int i = 0; i < 3; ++i) {
+        if (c->fcache_win[i]) ncclCommWindowDeregister(c->world, c->fcache_win[i]);
+        if (c->fcache_buf[i]) ncclMemFree(c->fcache_buf[i]);
+        c->fcache_win[i] = nullptr;
+        c->fcache_buf[i] = nullptr;
+    }
+    c->fcache_bytes = 0;
 }
 
 #define CUDA_TRY_F(c, x, what)                                  \

@@ -101,6 +101,7 @@ struct gcp_ctx {
     ncclComm_t world = nullptr;
     ncclComm_t slice[gcp::kMaxModes] = {nullptr};
     int slice_size[gcp::kMaxModes] = {0}, slice_rank[gcp::kMaxModes] = {0};
+    int slice_d = 0, slice_grid[gcp::kMaxModes] = {0};   // geometry the slice comms were split for
     bool ar_mode[gcp::kMaxModes] = {false};   // sync exchange of mode k: all-reduce (else RS/AG)
     // fused NVLink exchange (fused.cu): symmetric windows + device communicator
     bool fused = false, devcomm_ready = false;
@@ -113,6 +114,13 @@ struct gcp_ctx {
     ncclDevComm devcomm{};
     ncclWindow_t winA = nullptr, winG[2] = {nullptr, nullptr};
     void* d_G2 = nullptr;                         // second G buffer (iteration parity)
+    // windows of the previous model kept registered for the next one of the same
+    // size (a replace-ingest job skips the collective deregister / register)
+    void* fcache_buf[3] = {nullptr, nullptr, nullptr};
+    ncclWindow_t fcache_win[3] = {nullptr, nullptr, nullptr};
+    size_t fcache_bytes = 0;
+    size_t fwin_bytes = 0;                        // size of each live window
+    bool closing = false;                         // gcp_destroy: free everything
     void* twosided = nullptr;                     // row f3 scratch (twosided.cu)
     int fmem[gcp::kMaxModes][8] = {{0}}, fnmem[gcp::kMaxModes] = {0};
     int64_t tau = 0;
@@ -248,6 +256,7 @@ bool fused_possible(gcp_ctx* c);
 bool fused_use_multimem(const gcp_ctx* c);   // NVLS multicast for full-team modes
 gcp_status fused_alloc(gcp_ctx* c, size_t bytes);   // A, G, G2 as symmetric windows (collective)
 void fused_free(gcp_ctx* c);
+void fused_cache_release(gcp_ctx* c);   // collective: deregister the kept windows
 gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower);
 
 }  // namespace gcp

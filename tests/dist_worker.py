@@ -115,6 +115,18 @@ def main():
     for k in range(3):
         want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
         assert np.allclose(ctx.model_get(k), want, rtol=10 * TM, atol=TM), f"fit model k={k}"
+    # replace-ingest on the same context (a repeated job): the grid is unchanged, so
+    # the slice communicators and the symmetric windows are reused, not re-created;
+    # the fit must repeat the oracle's trajectory
+    ctx.tensor_create(dims, bs, bv)
+    ctx.model_init(R, 77)
+    _, rows2 = ctx.fit(fp)
+    assert len(rows2) == len(hist), (rows2, hist)
+    for r, h in zip(rows2, hist):
+        assert abs(r[2] - h[0]) <= 10 * TE * abs(h[0]), ("replace-ingest", r, h)
+    for k in range(3):
+        want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
+        assert np.allclose(ctx.model_get(k), want, rtol=10 * TM, atol=TM), f"replace-ingest fit model k={k}"
     ctx.close()
     dist.barrier()
     if rank == 0:
