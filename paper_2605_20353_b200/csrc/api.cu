@@ -180,6 +180,7 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     s.keys = c->d_keys;
     s.err_slot = c->d_err;
     s.it_dev = nullptr;
+    s.order = nullptr;
     if (c->capturing) {   // epoch graph: this launch's iteration relative to the replay's first
         s.it_dev = &c->d_step->it;
         s.it = it - c->graph_it0;
@@ -206,6 +207,8 @@ ModelArgs model_args(const gcp_ctx* c) {
 gcp_status ensure_partials(gcp_ctx* c, int n) {
     if (n <= c->partials_cap) return GCP_OK;
     gfree(c, c->d_partials);
+    gfree(c, c->d_ord);
+    gfree(c, c->d_ord_tmp);
     c->d_partials = nullptr;
     CUDA_TRY(c, gmalloc(c, &c->d_partials, sizeof(double) * (n + 1)), "partials");
     c->partials_cap = n;
@@ -620,6 +623,11 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         if (env) il = atoi(env) != 0 && c->P == 1 && c->mode == GCP_DIST_SYNC;
         c->ag_interleaved = il;
         c->ag_stride = il ? 2 * c->R_pad : c->R_pad;
+        // slot ordering by mode-1 position: pays when mode 1's A and G rows
+        // themselves spill out of L2 (c4, c5); GCP_SLOT_ORDER=0/1 overrides
+        const char* oenv = getenv("GCP_SLOT_ORDER");
+        const bool m1_spills = 2.0 * (double)c->rows[0] * (double)rb > 0.25 * (double)c->l2_bytes;
+        c->slot_order = oenv ? atoi(oenv) != 0 : m1_spills;
     }
     const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
     const bool use_fused = fused_possible(c);
@@ -823,8 +831,44 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     const ModelArgs m = model_args(c);
     const int with_loss = sampled_loss_out != nullptr;
     cudaEvent_t ev;
+    SampleArgs so = s;
+    if (c->slot_order && !two_sided(c)) {
+        // group this iteration's slots by mode-1 position (same sample set, other
+        // visiting order), so the K2 gathers / scatter-adds of one mode-1 row meet
+        // in L2 (kernels.cu launch_slot_order: a 3-launch counting sort)
+        const int64_t n = c->p_w + c->q_w;
+        if (n > c->ord_cap && !c->capturing) {
+            gfree(c, c->d_ord);
+            gfree(c, c->d_ord_tmp);
+            c->d_ord = nullptr;
+            c->d_ord_tmp = nullptr;
+            c->ord_cap = 0;
+            size_t tb = 0;
+            CUDA_TRY(c, launch_slot_order(c, s, nullptr, n, nullptr, &tb, nullptr), "slot order");
+            // a visiting-order optimisation only: without the memory for it, K2
+            // runs in slot order
+            if (gmalloc(c, &c->d_ord, slot_order_words(c, n) * 4) != cudaSuccess ||
+                gmalloc(c, &c->d_ord_tmp, tb) != cudaSuccess) {
+                cudaGetLastError();
+                gfree(c, c->d_ord);
+                gfree(c, c->d_ord_tmp);
+                c->d_ord = nullptr;
+                c->d_ord_tmp = nullptr;
+                c->slot_order = 0;
+            } else {
+                c->ord_tmp_bytes = tb;
+                c->ord_cap = n;
+            }
+        }
+        if (n <= c->ord_cap) {
+            prof_begin(c, PROF_OTHER, &ev);
+            size_t tb = c->ord_tmp_bytes;
+            CUDA_TRY(c, launch_slot_order(c, s, c->d_ord, c->ord_cap, c->d_ord_tmp, &tb, &so.order), "slot order");
+            prof_end(c, PROF_OTHER, ev);
+        }
+    }
     prof_begin(c, PROF_GRAD, &ev);
-    CUDA_TRY(c, launch_sample_kernel(c, s, m, loss, 0, !stratified, weight_nz(c, c->p_w), weight_z(c, c->q_w),
+    CUDA_TRY(c, launch_sample_kernel(c, so, m, loss, 0, !stratified, weight_nz(c, c->p_w), weight_z(c, c->q_w),
                                      with_loss, c->d_partials, c->grad_blocks),
              "gcp_loss_grad");
     prof_end(c, PROF_GRAD, ev);

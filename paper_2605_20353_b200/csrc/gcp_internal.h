@@ -54,6 +54,7 @@ struct SampleArgs {
     const uint32_t* it_dev;   // non-null inside a captured epoch graph: it = *it_dev + it (offset)
     const uint64_t* filter;   // blocked Bloom filter of the block's keys (4 u64 per 32-B sector), or null
     uint64_t filter_mask;     // sectors - 1 (power of two)
+    const uint32_t* order;    // gradient launches: slot processing order (null = slot order), see slot_order
 };
 
 // Epoch-graph replay state: the values of rate, t and it at the start of the
@@ -174,6 +175,13 @@ struct gcp_ctx {
     gcp::DevStep* d_step = nullptr;     // device step state read by K2 / Adam during replay
     gcp::DevStep* h_step = nullptr;     // pinned staging for the per-replay upload
     bool capturing = false;
+    // slot ordering (kernels.cu launch_slot_order): the gradient K2 visits its slots
+    // grouped by mode-1 position; buffers sized for ord_cap slots
+    uint32_t* d_ord = nullptr;          // slot_order_words(ord_cap) u32: bucket counts, offsets, order
+    void* d_ord_tmp = nullptr;
+    size_t ord_tmp_bytes = 0;
+    int64_t ord_cap = 0;
+    int slot_order = 0;                 // decided in gcp_model_init (GCP_SLOT_ORDER overrides)
     cudaGraphExec_t graph_exec = nullptr;
     double graph_key[8] = {0};
     double graph_seen[8] = {0};         // key of the last eager epoch: capture on the second sighting
@@ -220,6 +228,9 @@ void prof_end(gcp_ctx* c, int which, cudaEvent_t ev);
 cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss,
                                  int loss_mode, int semi_nz, double w_nz, double w_z, int with_loss,
                                  double* partials, int nblocks);
+size_t slot_order_words(const gcp_ctx* c, int64_t cap);
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, uint32_t* buf, int64_t cap, void* tmp,
+                              size_t* tmp_bytes, const uint32_t** order_out);
 cudaError_t launch_reduce_partials(gcp_ctx* c, const double* partials, int n, double* out);
 cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);

@@ -2,6 +2,11 @@
 // helper kernels (deterministic partial-sum reduction, scale, subtract).
 #include "kernels.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <string>
+
 namespace gcp {
 
 cudaError_t sample_kernel_f32(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
@@ -62,6 +67,128 @@ cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
         ia.goff[k] = k < c->d ? goff[k] : 0;
     }
     return c->prec == GCP_FP32 ? init_f32(c, ia, c->d_A) : init_f64(c, ia, c->d_A);
+}
+
+// Slot ordering for the gradient K2: a counting sort of the slots into
+// 2*kOrdB mode-1 position buckets -- nonzero slots by j (records are sorted
+// with i_1 most significant, so j order is i_1 order), zero slots by c_1 of the
+// attempt-0 candidate, each taken from the top bits of the Philox word
+// issue_sample scales into j or c_1 (device.cuh).  Order inside a bucket is arbitrary.
+// The sample set, and so the estimate, is unchanged; only the visiting order
+// changes, so that K2's gathers and scatter-adds of one mode-1 row meet in L2.
+// Three launches: per-CTA bucket histograms (shared-memory atomics), one
+// exclusive scan of the bucket-major [bucket][CTA] counts, and the scatter of
+// slot ids to their positions (each CTA re-draws the keys of its slot range).
+constexpr int kOrdBits = 12;
+constexpr int kOrdB = 1 << kOrdBits;
+constexpr int kOrdNB = 2 * kOrdB;
+constexpr int kOrdThreads = 512;
+
+__device__ __forceinline__ uint32_t slot_bucket(const SampleArgs& a, int64_t s) {
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    // j = mulhi(W, N) and c_1 = mulhi(W, I_1) are monotone in the Philox word W,
+    // so its top bits order the slots by j (nonzero) or c_1 (zero) -- no division
+    if (s < a.p) {
+        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, iter_word(a), k0, k1);
+        return (uint32_t)(w.w0 >> (64 - kOrdBits));
+    }
+    const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, iter_word(a), k0, k1);
+    return (uint32_t)kOrdB + (uint32_t)(w.w0 >> (64 - kOrdBits));
+}
+
+// radix variant (the default): 16-bit keys, the top 15 bits of W and the
+// stratum bit, sorted as (key, slot) pairs by cub (2 passes of 8 bits)
+__global__ void k_slot_keys16(const SampleArgs a, uint32_t* __restrict__ keys, uint32_t* __restrict__ slots) {
+    const int64_t total = a.p + a.q;
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const bool nz = s < a.p;
+        const U64x2 w = philox((uint32_t)(nz ? s : s - a.p), a.rank, (nz ? a.kind_nz : a.kind_z) << 28, iter_word(a),
+                               k0, k1);
+        keys[s] = ((uint32_t)(w.w0 >> 49) << 1) | (nz ? 0u : 1u);
+        slots[s] = (uint32_t)s;
+    }
+}
+
+__global__ void __launch_bounds__(kOrdThreads) k_slot_hist(const SampleArgs a, int64_t per,
+                                                            uint32_t* __restrict__ counts) {
+    __shared__ uint32_t h[kOrdNB];
+    for (int b = threadIdx.x; b < kOrdNB; b += kOrdThreads) h[b] = 0;
+    __syncthreads();
+    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, a.p + a.q);
+    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) atomicAdd(&h[slot_bucket(a, s)], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kOrdNB; b += kOrdThreads) counts[(size_t)b * gridDim.x + blockIdx.x] = h[b];
+}
+
+__global__ void __launch_bounds__(kOrdThreads) k_slot_scatter(const SampleArgs a, int64_t per,
+                                                               const uint32_t* __restrict__ offs,
+                                                               uint32_t* __restrict__ order) {
+    __shared__ uint32_t h[kOrdNB];
+    for (int b = threadIdx.x; b < kOrdNB; b += kOrdThreads) h[b] = offs[(size_t)b * gridDim.x + blockIdx.x];
+    __syncthreads();
+    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, a.p + a.q);
+    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads)
+        order[atomicAdd(&h[slot_bucket(a, s)], 1u)] = (uint32_t)s;
+}
+
+static int ord_ctas(const gcp_ctx* c) { return c->sm_count * 2; }
+
+// the radix order (16-bit keys) is finer than the counting sort's 2 x 4096
+// buckets: on c4 K2 2.85 vs 3.17 ms for 0.47 vs 0.29 ms of ordering, 2.48 vs
+// 2.39 epochs/s (profiles/r01_slotorder_*.json); GCP_SLOT_SORT=count selects the other
+static bool ord_radix() {
+    const char* e = getenv("GCP_SLOT_SORT");
+    return !(e && std::string(e) == "count");
+}
+
+size_t slot_order_words(const gcp_ctx* c, int64_t cap) {
+    return ord_radix() ? 4 * (size_t)cap : 2 * (size_t)kOrdNB * ord_ctas(c) + (size_t)cap;
+}
+
+static cudaError_t slot_order_radix(gcp_ctx* c, const SampleArgs& s, uint32_t* buf, int64_t cap, void* tmp,
+                                    size_t* tmp_bytes, const uint32_t** order_out) {
+    cub::DoubleBuffer<uint32_t> keys(buf, buf ? buf + cap : nullptr);
+    cub::DoubleBuffer<uint32_t> vals(buf ? buf + 2 * cap : nullptr, buf ? buf + 3 * cap : nullptr);
+    if (!tmp) return cub::DeviceRadixSort::SortPairs(nullptr, *tmp_bytes, keys, vals, (int)cap, 0, 16, c->stream);
+    const int64_t n = s.p + s.q;
+    const int nb = (int)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), (int64_t)c->sm_count * 8);
+    k_slot_keys16<<<nb, 256, 0, c->stream>>>(s, keys.Current(), vals.Current());
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    c->launches++;
+    e = cub::DeviceRadixSort::SortPairs(tmp, *tmp_bytes, keys, vals, (int)n, 0, 16, c->stream);
+    if (e != cudaSuccess) return e;
+    *order_out = vals.Current();
+    return cudaSuccess;
+}
+
+// buf: slot_order_words(c, cap) u32 (counts, offsets, order); tmp == nullptr
+// queries the scan's *tmp_bytes
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, uint32_t* buf, int64_t cap, void* tmp,
+                              size_t* tmp_bytes, const uint32_t** order_out) {
+    if (ord_radix()) return slot_order_radix(c, s, buf, cap, tmp, tmp_bytes, order_out);
+    const int nc = ord_ctas(c);
+    const int nbins = kOrdNB * nc;
+    uint32_t* counts = buf;
+    uint32_t* offs = buf ? buf + nbins : nullptr;
+    uint32_t* order = buf ? buf + 2 * (size_t)nbins : nullptr;
+    if (!tmp) return cub::DeviceScan::ExclusiveSum(nullptr, *tmp_bytes, counts, offs, nbins, c->stream);
+    const int64_t n = s.p + s.q;
+    if (n > cap) return cudaErrorInvalidValue;
+    const int64_t per = (n + nc - 1) / nc;
+    k_slot_hist<<<nc, kOrdThreads, 0, c->stream>>>(s, per, counts);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, counts, offs, nbins, c->stream);
+    if (e != cudaSuccess) return e;
+    k_slot_scatter<<<nc, kOrdThreads, 0, c->stream>>>(s, per, offs, order);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    c->launches += 2;
+    *order_out = order;
+    return cudaSuccess;
 }
 
 // Fixed-order sum of n fp64 partials (deterministic; one CTA).

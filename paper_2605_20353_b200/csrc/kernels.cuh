@@ -69,6 +69,11 @@ template <int D, int NV> struct SampleGeom {
     static constexpr int rowregs = small ? 4 : kRowRegBudget;
 };
 
+// position s of the visiting order -> slot (identity unless a slot order is given)
+__device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t s, int64_t total) {
+    return (a.order && s < total) ? (int64_t)__ldg(a.order + s) : s;
+}
+
 template <typename T, int D, int GL, int NV>
 __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
                                                    const KParams<T> kp) {
@@ -106,12 +111,12 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
     double lacc = 0.0;
     // software pipeline: the next chunk's record / first-bucket loads are in
     // flight while this chunk's rows are gathered and scattered
-    Pending<D> nxt = issue_sample<T, D>(sa, (warp0 << 5) + lane);
+    Pending<D> nxt = issue_sample<T, D>(sa, slot_at(sa, (warp0 << 5) + lane, total));
     for (int64_t chunk = warp0; chunk < nchunks; chunk += nwarps) {
         const int64_t s = (chunk << 5) + lane;
         const bool valid = s < total;
         const Pending<D> cur = nxt;
-        nxt = issue_sample<T, D>(sa, ((chunk + nwarps) << 5) + lane);
+        nxt = issue_sample<T, D>(sa, slot_at(sa, ((chunk + nwarps) << 5) + lane, total));
         Sample<T, D> smp;
         if (valid) smp = resolve_sample<T, D>(sa, cur);
         else {

@@ -147,6 +147,28 @@ def test_ag_layouts_agree(gcp, orc, interleave, monkeypatch):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("strategy", ["stratified", "semi"])
+def test_slot_order_same_gradient(gcp, orc, strategy, prec, monkeypatch):
+    """GCP_SLOT_ORDER=1: the gradient K2 visits its slots grouped by mode-1
+    position (a radix sort of the slots, kernels.cu).  Same sample set, so the
+    same gradient as the oracle's within the fp tolerance; p + q spans many
+    warps and a ragged tail."""
+    monkeypatch.setenv("GCP_SLOT_ORDER", "1")
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals, prec=prec)
+    t = orc.Tensor(dims, subs, vals)
+    for it, (p, q) in enumerate([(1000, 1000), (3333, 77), (0, 1501)]):
+        c.sample(strategy, p, q, 3001)
+        A = _model(c, 3)
+        c.loss_grad("poisson")
+        G = [c.grad_get(k) for k in range(3)]
+        Go, S, _ = orc.sampled_grad(t, A, "poisson", 3001, 0, it, p, q, strategy)
+        _grad_check(G, Go, S, TOL[prec], f"slot order {strategy}/{prec} p={p} q={q}")
+        c.adam_step(gcp.adam_params(rate=1e-2))   # resets G, advances the iteration counter
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
 @pytest.mark.parametrize("loss", LOSSES)
 def test_loss_estimate_parity(gcp, orc, loss, prec):
     dims = (20, 30, 40)
@@ -288,15 +310,18 @@ def test_sorted_membership_same_draws(gcp, orc, shape):
     _grad_check(G, Go, S, 1e-4, "sorted membership")
 
 
-@pytest.mark.parametrize("graphs,interleave", [("1", "0"), ("0", "0"), ("1", "1")])
-def test_fit_matches_oracle(gcp, orc, graphs, interleave, monkeypatch):
+@pytest.mark.parametrize("graphs,interleave,order", [("1", "0", "0"), ("0", "0", "0"), ("1", "1", "0"),
+                                                   ("1", "1", "1")])
+def test_fit_matches_oracle(gcp, orc, graphs, interleave, order, monkeypatch):
     """The epoch loop (annealing, R20) against oracle.fit, fp64, on a side
     stream: with GCP_GRAPHS=1 each epoch's iterations replay as one CUDA graph
     with the step state on the device; with 0 they launch one by one; and the
-    graph path with A/G rows interleaved (the layout c4 uses)."""
+    graph path with A/G rows interleaved (the layout c4 uses), also with the
+    slots visited in mode-1 order (captured prepass + radix sort)."""
     import torch
     monkeypatch.setenv("GCP_GRAPHS", graphs)
     monkeypatch.setenv("GCP_AG_INTERLEAVE", interleave)
+    monkeypatch.setenv("GCP_SLOT_ORDER", order)
     dims = (20, 30, 40)
     subs, vals = _tensor("poisson")
     stream = torch.cuda.Stream(0)
