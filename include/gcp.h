@@ -166,7 +166,8 @@ gcp_status gcp_dist_set_async(gcp_ctx* ctx, int64_t tau, const gcp_adam_params* 
  * duplicates, and builds the hash set of block-linearised keys (u64, or u128
  * when the block has >= 2^64 entries).  Replaces any previous tensor and drops
  * the model (both freed before the ingest; on failure the context has no
- * tensor).  Blocks; collective for nranks > 1 (global N and M checks). */
+ * tensor).  GCP_E_ARG if prod I_k does not fit in 128 bits.
+ * Blocks; collective for nranks > 1 (global N and M checks). */
 gcp_status gcp_tensor_create(gcp_ctx* ctx, int d, const int64_t* dims, int64_t nnz,
                              const int64_t* subs, const double* vals);
 
@@ -195,7 +196,12 @@ gcp_status gcp_tensor_contains(gcp_ctx* ctx, int64_t n, const int64_t* coords, i
  * a multiple of 4 columns) for this rank's block rows, moments B = C = 0 and
  * the gradient G = 0 (one contiguous array each), lambda = 1, and
  * fill A^(k) ~ U[0,1) by Philox (reading R12; identical on every rank and for
- * every grid).  Resets the Adam step t and the iteration counter to 0. */
+ * every grid).  Resets the Adam step t and the iteration counter to 0.
+ * Sync nranks > 1 with the fused NVLink exchange: A, G and a second G live in
+ * NCCL symmetric windows; on replacement, up to min(4 GiB, 1/32 of device
+ * memory) of the previous model's registered windows stay allocated (outside
+ * the allocation pool) for a next model of the same padded size, until that
+ * model or gcp_destroy. */
 gcp_status gcp_model_init(gcp_ctx* ctx, int R, uint64_t seed);
 
 /* Overwrite factor k's block rows (host, (hi_k-lo_k) x R doubles, row-major;
@@ -273,6 +279,21 @@ gcp_status gcp_fit(gcp_ctx* ctx, const gcp_fit_params* p, gcp_trace_fn trace, vo
                    double* final_est_loss);
 
 /* ---- instrumentation ----------------------------------------------------- */
+
+/* Layout choices the context made (all nullable; 0 without a model / tensor):
+ * A/G rows interleaved in one 128-B line (factors spill L2), gradient slots
+ * visited in mode-1 order (mode-1 rows spill L2; kernels.cu), L2 Bloom filter
+ * in front of the zero test.  For tests and benchmarks.  Does not block. */
+gcp_status gcp_layout(gcp_ctx* ctx, int* ag_interleaved, int* slot_order, int* filter);
+
+/* Test helper for the index map of reading R11 at N >= 2^32: the
+ * canonical nonzero index j of nonzero slots [first, first+count) (first+count
+ * <= 2^32) of iteration word `it`, rank word `rank`, kind 0, computed by the
+ * device draw path of the sample kernels with a pretend local nonzero count N
+ * (every draw reads record 0, so no tensor of N nonzeros is needed; needs a
+ * tensor with >= 1 nonzero).  j_out: count int64 (host).  Blocks. */
+gcp_status gcp_debug_nonzero_j(gcp_ctx* ctx, uint64_t seed, uint32_t rank, uint32_t it, int64_t N,
+                               int64_t first, int64_t count, int64_t* j_out);
 
 /* Counters: it (Philox iteration word), t (Adam steps), kernel launches made
  * by this library since creation (all nullable).  Does not block. */

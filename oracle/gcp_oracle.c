@@ -470,12 +470,12 @@ int orc_build_Y(const orc_tensor *t, int R, const double *lambda, const double *
 int orc_sampled_grad(const orc_tensor *t, int R, const double *lambda, const double *A_flat,
                      int loss, int strategy, uint64_t seed, uint32_t rank, uint32_t it,
                      int64_t p_w, int64_t q_w, double *G_flat, double *S_flat,
-                     double *loss_out, int64_t *err_slot)
+                     double *loss_out, double *loss_scale_out, int64_t *err_slot)
 {
     orc_model m; make_model(&m, t, R, lambda, A_flat);
     int d = t->d;
     int64_t coords[32];
-    double lsum = 0.0;
+    double lsum = 0.0, lscale = 0.0;
     if (p_w > 0 && t->N == 0) return ORC_E_NO_NONZEROS;
     if (q_w > 0 && strategy == ORC_STRATIFIED && block_M(t) == (u128)t->N) return ORC_E_NO_ZEROS;
     double w_nz = p_w > 0 ? weight_nz(t, p_w) : 0.0;
@@ -494,6 +494,7 @@ int orc_sampled_grad(const orc_tensor *t, int R, const double *lambda, const dou
         }
         mttkrp_entry(&m, t, coords, y, G_flat, ys, S_flat);
         lsum += w_nz * orc_loss_f(loss, x, mv);
+        if (loss_scale_out) lscale += fabs(w_nz) * f_scale(loss, x, mv, model_abs(&m, t, coords));
     }
     for (int64_t s = 0; s < q_w; ++s) {
         int a = draw_zero(t, seed, rank, KIND_GRAD_Z, it, (uint32_t)s, strategy == ORC_STRATIFIED, coords);
@@ -503,8 +504,10 @@ int orc_sampled_grad(const orc_tensor *t, int R, const double *lambda, const dou
         double ys = S_flat ? fabs(w_z) * df_scale(loss, 0.0, mv, model_abs(&m, t, coords)) : 0.0;
         mttkrp_entry(&m, t, coords, y, G_flat, ys, S_flat);
         lsum += w_z * orc_loss_f(loss, 0.0, mv);
+        if (loss_scale_out) lscale += fabs(w_z) * f_scale(loss, 0.0, mv, model_abs(&m, t, coords));
     }
     if (loss_out) *loss_out = lsum;
+    if (loss_scale_out) *loss_scale_out = lscale;   /* tolerance scale of lsum (C18), as in orc_loss_estimate */
     return ORC_OK;
 }
 

@@ -85,7 +85,7 @@ def lib():
         L.orc_build_Y.argtypes = [vp, C.c_int, dp, dp, C.c_int, C.c_int, C.c_uint64, C.c_uint32,
                                   C.c_uint32, C.c_int64, C.c_int64, i64p, dp, i64p]
         L.orc_sampled_grad.argtypes = [vp, C.c_int, dp, dp, C.c_int, C.c_int, C.c_uint64, C.c_uint32,
-                                       C.c_uint32, C.c_int64, C.c_int64, dp, dp, dp, i64p]
+                                       C.c_uint32, C.c_int64, C.c_int64, dp, dp, dp, dp, i64p]
         L.orc_loss_estimate.argtypes = [vp, C.c_int, dp, dp, C.c_int, C.c_uint64, C.c_uint32,
                                         C.c_int64, C.c_int64, dp, dp, i64p]
         L.orc_full_loss.argtypes = [vp, C.c_int, dp, dp, C.c_int, dp]
@@ -268,21 +268,23 @@ def sample_export(t, stratum, seed, rank, it, n_stratum, first, count,
 
 
 def sampled_grad(t, A, loss, seed, rank, it, p_w, q_w, strategy="stratified", lam=None,
-                 with_scale=True):
+                 with_scale=True, loss_scale=False):
     """Fused Sampling-MTTKRP for one rank.  Returns (G, S, sampled loss)
-    with G, S lists of block-row matrices."""
+    with G, S lists of block-row matrices; with loss_scale=True also the
+    rounding scale sum |w f| of the sampled loss (tolerance only, C18)."""
     R = A[0].shape[1]
     Af, la = _f64(t.block_rows(A)), _lam(lam, R)
     G = np.zeros_like(Af)
     S = np.zeros_like(Af) if with_scale else None
-    ls = C.c_double(0)
+    ls, lsc = C.c_double(0), C.c_double(0)
     err = C.c_int64(-1)
     st = lib().orc_sampled_grad(t._h, R, _p(la, C.c_double), _p(Af, C.c_double), LOSSES[loss],
                                 STRATEGIES[strategy], seed, rank, it, p_w, q_w,
                                 _p(G, C.c_double), _p(S, C.c_double) if with_scale else None,
-                                C.byref(ls), C.byref(err))
+                                C.byref(ls), C.byref(lsc) if loss_scale else None, C.byref(err))
     _check(st, f"slot {err.value}")
-    return t.split_rows(G, R), (t.split_rows(S, R) if with_scale else None), ls.value
+    out = (t.split_rows(G, R), (t.split_rows(S, R) if with_scale else None), ls.value)
+    return out + (lsc.value,) if loss_scale else out
 
 
 def build_Y(t, A, loss, seed, rank, it, p_w, q_w, strategy="stratified", lam=None):
@@ -336,6 +338,41 @@ def full_grad(t, A, loss, lam=None):
     _check(lib().orc_full_grad(t._h, R, _p(la, C.c_double), _p(Af, C.c_double), LOSSES[loss],
                                _p(G, C.c_double)), "full_grad guard")
     return t.split_rows(G, R)
+
+
+def poisson_exact_grad(subs, vals, A, lam=None, chunk=4_000_000):
+    """Exact gradient dF/dA^(k) of the Poisson GCP objective (P:282-296 with the
+    loss of reading R3) at any scale, in O(N d R): f'(0, m) = 1 for every entry,
+    so summing over all M entries gives
+        G^(k)[i, r] = lam_r prod_{j != k} colsum_r(A^(j))
+                      - sum_{nonzeros with i_k = i} x / (m + eps) lam_r prod_{j != k} A^(j)[i_j, r]
+    (SURVEY C17 "Poisson identity"; pinned against enumeration in
+    tests/test_oracle_math.py).  Global coordinates and global factors; fp64."""
+    d, R = len(A), A[0].shape[1]
+    lam = np.ones(R) if lam is None else np.asarray(lam, np.float64)
+    A = [np.asarray(a, np.float64) for a in A]
+    cs = [a.sum(axis=0) for a in A]
+    G = []
+    for k in range(d):
+        dense = lam.copy()
+        for j in range(d):
+            if j != k:
+                dense = dense * cs[j]
+        G.append(np.tile(dense, (A[k].shape[0], 1)))
+    subs = np.asarray(subs)
+    vals = np.asarray(vals, np.float64)
+    for c0 in range(0, len(vals), chunk):
+        sb = subs[c0:c0 + chunk].astype(np.int64)
+        rows = [A[k][sb[:, k]] for k in range(d)]
+        full = lam * np.prod(rows, axis=0)                       # lam_r prod_k a_k[r]
+        m = full.sum(axis=1)
+        y = -vals[c0:c0 + chunk] / (m + 1e-10)
+        for k in range(d):
+            others = lam * np.prod([rows[j] for j in range(d) if j != k], axis=0)   # no division
+            z = y[:, None] * others
+            for r in range(R):
+                G[k][:, r] += np.bincount(sb[:, k], weights=z[:, r], minlength=A[k].shape[0])
+    return G
 
 
 def adam(A, G, B, Cm, t, alpha, beta1=0.9, beta2=0.999, eps=1e-8, lower=-math.inf):

@@ -204,11 +204,21 @@ ModelArgs model_args(const gcp_ctx* c) {
     return m;
 }
 
+// the slot-order buffers (their table T is per tensor: dropped with the tensor)
+void ord_free(gcp_ctx* c) {
+    graph_drop(c);
+    gfree(c, c->d_ord_buf);
+    c->d_ord_buf = nullptr;
+    c->d_ord_T = nullptr;
+    c->d_ord_cnt = nullptr;
+    c->d_ord = nullptr;
+    c->d_ord_key = nullptr;
+    c->ord_cap = 0;
+}
+
 gcp_status ensure_partials(gcp_ctx* c, int n) {
     if (n <= c->partials_cap) return GCP_OK;
     gfree(c, c->d_partials);
-    gfree(c, c->d_ord);
-    gfree(c, c->d_ord_tmp);
     c->d_partials = nullptr;
     CUDA_TRY(c, gmalloc(c, &c->d_partials, sizeof(double) * (n + 1)), "partials");
     c->partials_cap = n;
@@ -366,6 +376,7 @@ void gcp_destroy(gcp_ctx* c) {
     c->closing = true;
     free_model(c);
     fused_cache_release(c);
+    ord_free(c);
     gfree(c, c->d_rec);
     gfree(c, c->d_hash);
     gfree(c, c->d_keys);
@@ -452,6 +463,16 @@ gcp_status gcp_tensor_create(gcp_ctx* c, int d, const int64_t* dims, int64_t nnz
             b[k] = rem % grid[k];
             rem /= grid[k];
         }
+        // M = prod I_k must be representable in u128 (SPEC S:26 errors on an
+        // overflowing M_tot); the block's M is at most that
+        unsigned __int128 Mg = 1;
+        for (int k = 0; k < d; ++k) {
+            if (Mg > (~(unsigned __int128)0) / (unsigned __int128)dims[k]) {
+                delete g;
+                return set_error(GCP_E_ARG, "gcp_tensor_create: prod I_k overflows 128 bits");
+            }
+            Mg *= (unsigned __int128)dims[k];
+        }
         g->M = 1;
         for (int k = 0; k < d; ++k) {
             const int64_t ck = (dims[k] + grid[k] - 1) / grid[k];
@@ -465,6 +486,7 @@ gcp_status gcp_tensor_create(gcp_ctx* c, int d, const int64_t* dims, int64_t nnz
     // scratch reuses their memory (the pool keeps it mapped) instead of growing
     // past them.  A failed ingest leaves the context without a tensor.
     free_model(c);
+    ord_free(c);
     gfree(c, c->d_rec);
     gfree(c, c->d_hash);
     gfree(c, c->d_keys);
@@ -832,38 +854,28 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     const int with_loss = sampled_loss_out != nullptr;
     cudaEvent_t ev;
     SampleArgs so = s;
-    if (c->slot_order && !two_sided(c)) {
+    // slot ids are u32: beyond 2^32 slots per rank K2 runs in slot order
+    const int64_t n_slots = c->p_w + c->q_w;
+    if (c->slot_order && !two_sided(c) && n_slots < ((int64_t)1 << 32)) {
         // group this iteration's slots by mode-1 position (same sample set, other
         // visiting order), so the K2 gathers / scatter-adds of one mode-1 row meet
-        // in L2 (kernels.cu launch_slot_order: a 3-launch counting sort)
-        const int64_t n = c->p_w + c->q_w;
-        if (n > c->ord_cap && !c->capturing) {
-            gfree(c, c->d_ord);
-            gfree(c, c->d_ord_tmp);
-            c->d_ord = nullptr;
-            c->d_ord_tmp = nullptr;
-            c->ord_cap = 0;
-            size_t tb = 0;
-            CUDA_TRY(c, launch_slot_order(c, s, nullptr, n, nullptr, &tb, nullptr), "slot order");
+        // in L2 (kernels.cu launch_slot_order: a hand-written 3-launch counting sort)
+        if (n_slots > c->ord_cap && !c->capturing) {
+            ord_free(c);
             // a visiting-order optimisation only: without the memory for it, K2
             // runs in slot order
-            if (gmalloc(c, &c->d_ord, slot_order_words(c, n) * 4) != cudaSuccess ||
-                gmalloc(c, &c->d_ord_tmp, tb) != cudaSuccess) {
+            if (gmalloc(c, &c->d_ord_buf, slot_order_bytes(n_slots)) != cudaSuccess) {
                 cudaGetLastError();
-                gfree(c, c->d_ord);
-                gfree(c, c->d_ord_tmp);
-                c->d_ord = nullptr;
-                c->d_ord_tmp = nullptr;
+                c->d_ord_buf = nullptr;
                 c->slot_order = 0;
             } else {
-                c->ord_tmp_bytes = tb;
-                c->ord_cap = n;
+                CUDA_TRY(c, slot_order_init(c, c->d_ord_buf, n_slots), "slot order");
+                c->ord_cap = n_slots;
             }
         }
-        if (n <= c->ord_cap) {
+        if (c->slot_order && n_slots <= c->ord_cap) {
             prof_begin(c, PROF_OTHER, &ev);
-            size_t tb = c->ord_tmp_bytes;
-            CUDA_TRY(c, launch_slot_order(c, s, c->d_ord, c->ord_cap, c->d_ord_tmp, &tb, &so.order), "slot order");
+            CUDA_TRY(c, launch_slot_order(c, s, &so.order), "slot order");
             prof_end(c, PROF_OTHER, ev);
         }
     }
@@ -1143,6 +1155,42 @@ gcp_status gcp_dist_features(gcp_ctx* c, int* fused_out, int* multimem_out) {
     int mm = 0;
     for (int k = 0; k < c->d; ++k) mm |= fused_use_multimem(c) && c->fnmem[k] == c->P;
     if (multimem_out) *multimem_out = mm;
+    return GCP_OK;
+}
+
+gcp_status gcp_layout(gcp_ctx* c, int* ag_interleaved, int* slot_order, int* filter) {
+    ENTER(c);
+    if (ag_interleaved) *ag_interleaved = c->have_model && c->ag_interleaved ? 1 : 0;
+    if (slot_order) *slot_order = c->have_model && c->slot_order ? 1 : 0;
+    if (filter) *filter = c->have_tensor && c->filter_sectors ? 1 : 0;
+    return GCP_OK;
+}
+
+gcp_status gcp_debug_nonzero_j(gcp_ctx* c, uint64_t seed, uint32_t rank, uint32_t it, int64_t N, int64_t first,
+                               int64_t count, int64_t* j_out) {
+    ENTER(c);
+    if (!c->have_tensor || c->N < 1) return set_error(GCP_E_STATE, "gcp_debug_nonzero_j: need a tensor with nonzeros");
+    if (N < 1 || first < 0 || count < 0 || first + count > ((int64_t)1 << 32) || !j_out)
+        return set_error(GCP_E_ARG, "gcp_debug_nonzero_j: args");
+    if (count == 0) return GCP_OK;
+    // the device draw path (issue_sample + resolve_sample) with a pretend nonzero
+    // count N; a record stride of 0 points every draw at record 0, so no tensor
+    // of N nonzeros is needed
+    SampleArgs s = sample_args(c, first + count, 0, seed, it, KIND_GRAD_NZ, KIND_GRAD_Z, 1);
+    s.rank = rank;
+    s.N = N;
+    s.rec_words = 0;
+    int64_t *d_subs = nullptr, *d_j = nullptr, *d_lo = nullptr;
+    CUDA_TRY(c, gmalloc(c, &d_subs, sizeof(int64_t) * count * c->d), "debug_j");
+    CUDA_TRY(c, gmalloc(c, &d_j, sizeof(int64_t) * count), "debug_j");
+    CUDA_TRY(c, gmalloc(c, &d_lo, sizeof(int64_t) * kMaxModes), "debug_j");
+    CUDA_TRY(c, cudaMemsetAsync(d_lo, 0, sizeof(int64_t) * kMaxModes, c->stream), "debug_j");
+    CUDA_TRY(c, launch_export(c, s, 0, first, count, d_lo, d_subs, d_j, nullptr), "debug_j");
+    CUDA_TRY(c, cudaMemcpyAsync(j_out, d_j, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c->stream), "debug_j");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), "debug_j");
+    gfree(c, d_subs);
+    gfree(c, d_j);
+    gfree(c, d_lo);
     return GCP_OK;
 }
 

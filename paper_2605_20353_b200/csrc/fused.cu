@@ -328,10 +328,18 @@ void fused_free(gcp_ctx* c) {
     ncclWindow_t* wins[3] = {&c->winA, &c->winG[0], &c->winG[1]};
     cudaStreamSynchronize(c->stream);
     fused_cache_release(c);
-    // keep up to kFusedCacheMax of registered windows for the next model of the
-    // same size (replace-ingest jobs skip the collective deregister / register)
+    // keep up to min(kFusedCacheMax, 1/32 of device memory) of registered
+    // windows for the next model of the same size (replace-ingest jobs skip the
+    // collective deregister / register).  The decision must agree on every rank
+    // (deregistration is collective): it depends only on the symmetric window
+    // size and the device's total memory, never on its free memory.  The kept
+    // windows live outside the allocation pool until the next model of the same
+    // size or gcp_destroy (include/gcp.h, gcp_model_init).
     const size_t wb = c->fwin_bytes;
-    const bool keep = !c->closing && 3 * wb <= kFusedCacheMax && *wins[0] && *wins[1] && *wins[2];
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t cap = std::min(kFusedCacheMax, tot / 32);
+    const bool keep = !c->closing && 3 * wb <= cap && *wins[0] && *wins[1] && *wins[2];
     for (int i = 0; i < 3; ++i) {
         if (keep) {
             c->fcache_buf[i] = *bufs[i];

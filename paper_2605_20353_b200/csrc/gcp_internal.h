@@ -176,10 +176,12 @@ struct gcp_ctx {
     gcp::DevStep* h_step = nullptr;     // pinned staging for the per-replay upload
     bool capturing = false;
     // slot ordering (kernels.cu launch_slot_order): the gradient K2 visits its slots
-    // grouped by mode-1 position; buffers sized for ord_cap slots
-    uint32_t* d_ord = nullptr;          // slot_order_words(ord_cap) u32: bucket counts, offsets, order
-    void* d_ord_tmp = nullptr;
-    size_t ord_tmp_bytes = 0;
+    // grouped by mode-1 position; one allocation (d_ord_buf) sized for ord_cap slots
+    void* d_ord_buf = nullptr;
+    int64_t* d_ord_T = nullptr;         // per-tensor bucket -> first record table (kOrdB + 1)
+    uint32_t* d_ord_cnt = nullptr;      // bucket totals, cursors
+    uint32_t* d_ord = nullptr;          // visiting order (slot ids)
+    uint16_t* d_ord_key = nullptr;      // bucket per slot
     int64_t ord_cap = 0;
     int slot_order = 0;                 // decided in gcp_model_init (GCP_SLOT_ORDER overrides)
     cudaGraphExec_t graph_exec = nullptr;
@@ -228,9 +230,9 @@ void prof_end(gcp_ctx* c, int which, cudaEvent_t ev);
 cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss,
                                  int loss_mode, int semi_nz, double w_nz, double w_z, int with_loss,
                                  double* partials, int nblocks);
-size_t slot_order_words(const gcp_ctx* c, int64_t cap);
-cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, uint32_t* buf, int64_t cap, void* tmp,
-                              size_t* tmp_bytes, const uint32_t** order_out);
+size_t slot_order_bytes(int64_t cap);
+cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap);   // carve buffers, build the per-tensor table
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out);
 cudaError_t launch_reduce_partials(gcp_ctx* c, const double* partials, int n, double* out);
 cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);

@@ -2,9 +2,6 @@
 // helper kernels (deterministic partial-sum reduction, scale, subtract).
 #include "kernels.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include <string>
 
 namespace gcp {
@@ -69,126 +66,182 @@ cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
     return c->prec == GCP_FP32 ? init_f32(c, ia, c->d_A) : init_f64(c, ia, c->d_A);
 }
 
-// Slot ordering for the gradient K2: a counting sort of the slots into
-// 2*kOrdB mode-1 position buckets -- nonzero slots by j (records are sorted
-// with i_1 most significant, so j order is i_1 order), zero slots by c_1 of the
-// attempt-0 candidate, each taken from the top bits of the Philox word
-// issue_sample scales into j or c_1 (device.cuh).  Order inside a bucket is arbitrary.
-// The sample set, and so the estimate, is unchanged; only the visiting order
-// changes, so that K2's gathers and scatter-adds of one mode-1 row meet in L2.
-// Three launches: per-CTA bucket histograms (shared-memory atomics), one
-// exclusive scan of the bucket-major [bucket][CTA] counts, and the scatter of
-// slot ids to their positions (each CTA re-draws the keys of its slot range).
+// Slot ordering for the gradient K2 (DRAM-resident mode-1 rows: c4, c5): a
+// hand-written counting sort of the iteration's slots into kOrdB buckets of
+// mode-1 position, nonzero and zero slots interleaved (a bucket holds the
+// nonzero slots whose record lies in a mode-1 row range AND the zero slots
+// whose attempt-0 candidate lies in the same range, so K2 fills the A|G lines
+// of a row range once per iteration, not once per stratum).  The sample set,
+// and so the estimate, is unchanged; only the visiting order changes, so that
+// K2's gathers and scatter-adds of one mode-1 row meet in L2.
+//   k_ord_hist     Philox word -> bucket (nonzero: j = mulhi(W, N), then the
+//                  bucket whose record range [T[b], T[b+1]) holds j, by binary
+//                  search of the per-tensor table T in shared memory; zero:
+//                  c_1 = mulhi(W, I_1), bucket floor(c_1 B / I_1)); u16 key per
+//                  slot; shared-memory histogram; one global atomicAdd per
+//                  (CTA, bucket)
+//   k_ord_scan     one CTA: exclusive scan of the bucket totals -> cursors;
+//                  totals reset for the next iteration
+//   k_ord_scatter  per CTA: histogram of its keys again, one atomicAdd per
+//                  (CTA, bucket) reserves its run, slot ids scattered into it
+// Order inside a bucket is arbitrary (and run to run: CTAs reserve in arrival
+// order), which only moves the fp32 atomic summation order.
 constexpr int kOrdBits = 12;
 constexpr int kOrdB = 1 << kOrdBits;
-constexpr int kOrdNB = 2 * kOrdB;
-constexpr int kOrdThreads = 512;
+constexpr int kOrdThreads = 1024;
+constexpr size_t kOrdSmem = kOrdB * sizeof(uint32_t) + (kOrdB + 1) * sizeof(int64_t);
 
-__device__ __forceinline__ uint32_t slot_bucket(const SampleArgs& a, int64_t s) {
-    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-    // j = mulhi(W, N) and c_1 = mulhi(W, I_1) are monotone in the Philox word W,
-    // so its top bits order the slots by j (nonzero) or c_1 (zero) -- no division
-    if (s < a.p) {
-        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, iter_word(a), k0, k1);
-        return (uint32_t)(w.w0 >> (64 - kOrdBits));
+// T[b] = first canonical record whose c_1 >= ceil(b I_1 / B), b = 0..B (T[B] = N):
+// records are sorted with i_1 most significant (reading R15)
+__global__ void k_ord_table(const uint32_t* __restrict__ rec, int rec_words, int val_words, int64_t N, uint32_t I1,
+                            int64_t* __restrict__ T) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > kOrdB) return;
+    const uint64_t row = ((uint64_t)b * I1 + kOrdB - 1) >> kOrdBits;
+    int64_t lo = 0, hi = N;
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (rec[mid * rec_words + val_words] < row) lo = mid + 1;
+        else hi = mid;
     }
-    const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, iter_word(a), k0, k1);
-    return (uint32_t)kOrdB + (uint32_t)(w.w0 >> (64 - kOrdBits));
+    T[b] = lo;
 }
 
-// radix variant (the default): 16-bit keys, the top 15 bits of W and the
-// stratum bit, sorted as (key, slot) pairs by cub (2 passes of 8 bits)
-__global__ void k_slot_keys16(const SampleArgs a, uint32_t* __restrict__ keys, uint32_t* __restrict__ slots) {
-    const int64_t total = a.p + a.q;
+__global__ void __launch_bounds__(kOrdThreads) k_ord_hist(const SampleArgs a, const int64_t* __restrict__ T,
+                                                         int64_t per, uint16_t* __restrict__ keys,
+                                                         uint32_t* __restrict__ totals) {
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    int64_t* sT = reinterpret_cast<int64_t*>(ord_smem);
+    uint32_t* h = reinterpret_cast<uint32_t*>(sT + kOrdB + 1);
+    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads) h[b] = 0;
+    for (int b = threadIdx.x; b <= kOrdB; b += kOrdThreads) sT[b] = T[b];
+    __syncthreads();
     const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total;
-         s += (int64_t)gridDim.x * blockDim.x) {
-        const bool nz = s < a.p;
-        const U64x2 w = philox((uint32_t)(nz ? s : s - a.p), a.rank, (nz ? a.kind_nz : a.kind_z) << 28, iter_word(a),
-                               k0, k1);
-        keys[s] = ((uint32_t)(w.w0 >> 49) << 1) | (nz ? 0u : 1u);
-        slots[s] = (uint32_t)s;
+    const uint32_t it = iter_word(a);
+    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, a.p + a.q);
+    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) {
+        uint32_t b;
+        if (s < a.p) {
+            const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, it, k0, k1);
+            const int64_t j = (int64_t)range_map(w.w0, (uint64_t)a.N);
+            uint32_t lo = 0, hi = kOrdB;          // largest b with T[b] <= j (T[0] = 0 <= j < T[B] = N)
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sT[mid] <= j) lo = mid;
+                else hi = mid;
+            }
+            b = lo;
+        } else {
+            const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, it, k0, k1);
+            const uint64_t c1 = range_map(w.w0, a.bdim[0]);
+            b = (uint32_t)((c1 << kOrdBits) / a.bdim[0]);
+        }
+        keys[s] = (uint16_t)b;
+        atomicAdd(&h[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads)
+        if (h[b]) atomicAdd(&totals[b], h[b]);
+}
+
+__global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__ totals, uint32_t* __restrict__ cursor) {
+    constexpr int PER = kOrdB / kOrdThreads;
+    __shared__ uint32_t wsum[kOrdThreads / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint32_t v[PER], run = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        v[i] = totals[t * PER + i];
+        totals[t * PER + i] = 0;
+        run += v[i];
+    }
+    uint32_t incl = run;   // inclusive warp scan of the per-thread sums
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t x = lane < kOrdThreads / 32 ? wsum[lane] : 0, xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        if (lane < kOrdThreads / 32) wsum[lane] = xi - x;   // exclusive prefix of the warp totals
+    }
+    __syncthreads();
+    uint32_t base = wsum[w] + incl - run;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        cursor[t * PER + i] = base;
+        base += v[i];
     }
 }
 
-__global__ void __launch_bounds__(kOrdThreads) k_slot_hist(const SampleArgs a, int64_t per,
-                                                            uint32_t* __restrict__ counts) {
-    __shared__ uint32_t h[kOrdNB];
-    for (int b = threadIdx.x; b < kOrdNB; b += kOrdThreads) h[b] = 0;
+__global__ void __launch_bounds__(kOrdThreads) k_ord_scatter(const uint16_t* __restrict__ keys, int64_t n,
+                                                            int64_t per, uint32_t* __restrict__ cursor,
+                                                            uint32_t* __restrict__ order) {
+    __shared__ uint32_t h[kOrdB];
+    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads) h[b] = 0;
     __syncthreads();
-    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, a.p + a.q);
-    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) atomicAdd(&h[slot_bucket(a, s)], 1u);
+    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, n);
+    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) atomicAdd(&h[keys[s]], 1u);
     __syncthreads();
-    for (int b = threadIdx.x; b < kOrdNB; b += kOrdThreads) counts[(size_t)b * gridDim.x + blockIdx.x] = h[b];
-}
-
-__global__ void __launch_bounds__(kOrdThreads) k_slot_scatter(const SampleArgs a, int64_t per,
-                                                               const uint32_t* __restrict__ offs,
-                                                               uint32_t* __restrict__ order) {
-    __shared__ uint32_t h[kOrdNB];
-    for (int b = threadIdx.x; b < kOrdNB; b += kOrdThreads) h[b] = offs[(size_t)b * gridDim.x + blockIdx.x];
+    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads)
+        if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);   // this CTA's run of bucket b
     __syncthreads();
-    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, a.p + a.q);
-    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads)
-        order[atomicAdd(&h[slot_bucket(a, s)], 1u)] = (uint32_t)s;
+    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) order[atomicAdd(&h[keys[s]], 1u)] = (uint32_t)s;
 }
 
-static int ord_ctas(const gcp_ctx* c) { return c->sm_count * 2; }
-
-// the radix order (16-bit keys) is finer than the counting sort's 2 x 4096
-// buckets: on c4 K2 2.85 vs 3.17 ms for 0.47 vs 0.29 ms of ordering, 2.48 vs
-// 2.39 epochs/s (profiles/r01_slotorder_*.json); GCP_SLOT_SORT=count selects the other
-static bool ord_radix() {
-    const char* e = getenv("GCP_SLOT_SORT");
-    return !(e && std::string(e) == "count");
+size_t slot_order_bytes(int64_t cap) {
+    return (size_t)cap * (sizeof(uint32_t) + sizeof(uint16_t)) + 2 * kOrdB * sizeof(uint32_t) +
+           (kOrdB + 1) * sizeof(int64_t) + 64;
 }
 
-size_t slot_order_words(const gcp_ctx* c, int64_t cap) {
-    return ord_radix() ? 4 * (size_t)cap : 2 * (size_t)kOrdNB * ord_ctas(c) + (size_t)cap;
-}
-
-static cudaError_t slot_order_radix(gcp_ctx* c, const SampleArgs& s, uint32_t* buf, int64_t cap, void* tmp,
-                                    size_t* tmp_bytes, const uint32_t** order_out) {
-    cub::DoubleBuffer<uint32_t> keys(buf, buf ? buf + cap : nullptr);
-    cub::DoubleBuffer<uint32_t> vals(buf ? buf + 2 * cap : nullptr, buf ? buf + 3 * cap : nullptr);
-    if (!tmp) return cub::DeviceRadixSort::SortPairs(nullptr, *tmp_bytes, keys, vals, (int)cap, 0, 16, c->stream);
-    const int64_t n = s.p + s.q;
-    const int nb = (int)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), (int64_t)c->sm_count * 8);
-    k_slot_keys16<<<nb, 256, 0, c->stream>>>(s, keys.Current(), vals.Current());
-    cudaError_t e = cudaGetLastError();
+// Carve the order buffers out of one allocation of slot_order_bytes(cap) and
+// build the per-tensor table T (once per tensor).
+cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap) {
+    char* p = static_cast<char*>(buf);
+    c->d_ord_T = reinterpret_cast<int64_t*>(p);
+    p += (kOrdB + 1) * sizeof(int64_t);
+    c->d_ord_cnt = reinterpret_cast<uint32_t*>(p);
+    p += 2 * kOrdB * sizeof(uint32_t);
+    c->d_ord = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)cap * sizeof(uint32_t);
+    c->d_ord_key = reinterpret_cast<uint16_t*>(p);
+    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, 2 * kOrdB * sizeof(uint32_t), c->stream);
     if (e != cudaSuccess) return e;
+    k_ord_table<<<(kOrdB + 1 + 255) / 256, 256, 0, c->stream>>>(c->d_rec, c->rec_words, c->val_words, c->N,
+                                                                (uint32_t)(c->hi[0] - c->lo[0]), c->d_ord_T);
     c->launches++;
-    e = cub::DeviceRadixSort::SortPairs(tmp, *tmp_bytes, keys, vals, (int)n, 0, 16, c->stream);
-    if (e != cudaSuccess) return e;
-    *order_out = vals.Current();
-    return cudaSuccess;
+    return cudaGetLastError();
 }
 
-// buf: slot_order_words(c, cap) u32 (counts, offsets, order); tmp == nullptr
-// queries the scan's *tmp_bytes
-cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, uint32_t* buf, int64_t cap, void* tmp,
-                              size_t* tmp_bytes, const uint32_t** order_out) {
-    if (ord_radix()) return slot_order_radix(c, s, buf, cap, tmp, tmp_bytes, order_out);
-    const int nc = ord_ctas(c);
-    const int nbins = kOrdNB * nc;
-    uint32_t* counts = buf;
-    uint32_t* offs = buf ? buf + nbins : nullptr;
-    uint32_t* order = buf ? buf + 2 * (size_t)nbins : nullptr;
-    if (!tmp) return cub::DeviceScan::ExclusiveSum(nullptr, *tmp_bytes, counts, offs, nbins, c->stream);
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_ord_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOrdSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
     const int64_t n = s.p + s.q;
-    if (n > cap) return cudaErrorInvalidValue;
+    if (n == 0) {
+        *order_out = c->d_ord;
+        return cudaSuccess;
+    }
+    const int nc = c->sm_count;
     const int64_t per = (n + nc - 1) / nc;
-    k_slot_hist<<<nc, kOrdThreads, 0, c->stream>>>(s, per, counts);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, counts, offs, nbins, c->stream);
-    if (e != cudaSuccess) return e;
-    k_slot_scatter<<<nc, kOrdThreads, 0, c->stream>>>(s, per, offs, order);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    c->launches += 2;
-    *order_out = order;
-    return cudaSuccess;
+    uint32_t* totals = c->d_ord_cnt;
+    uint32_t* cursor = c->d_ord_cnt + kOrdB;
+    k_ord_hist<<<nc, kOrdThreads, kOrdSmem, c->stream>>>(s, c->d_ord_T, per, c->d_ord_key, totals);
+    k_ord_scan<<<1, kOrdThreads, 0, c->stream>>>(totals, cursor);
+    k_ord_scatter<<<nc, kOrdThreads, 0, c->stream>>>(c->d_ord_key, n, per, cursor, c->d_ord);
+    c->launches += 3;
+    *order_out = c->d_ord;
+    return cudaGetLastError();
 }
 
 // Fixed-order sum of n fp64 partials (deterministic; one CTA).

@@ -33,7 +33,7 @@ SYMBOLS = ["gcp_create", "gcp_destroy", "gcp_last_error", "gcp_grid_plan", "gcp_
            "gcp_model_get", "gcp_sample", "gcp_sample_export", "gcp_loss_grad", "gcp_grad_get",
            "gcp_adam_step", "gcp_loss_estimate", "gcp_fit_begin", "gcp_fit_epoch", "gcp_fit",
            "gcp_counters", "gcp_profile_enable", "gcp_profile_get", "gcp_set_membership",
-           "gcp_dist_features"]
+           "gcp_dist_features", "gcp_layout", "gcp_debug_nonzero_j"]
 MEMBERSHIP = {"hash": 0, "sorted": 1}
 
 
@@ -90,6 +90,8 @@ def load():
         "gcp_fit": [vp, C.POINTER(FitParams), TRACE_FN, vp, dp],
         "gcp_counters": [vp, C.POINTER(C.c_uint32), i64p, i64p],
         "gcp_dist_features": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "gcp_layout": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "gcp_debug_nonzero_j": [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int64, C.c_int64, C.c_int64, i64p],
         "gcp_profile_enable": [vp, C.c_int],
         "gcp_profile_get": [vp, C.c_int, dp, i64p, C.c_int],
         "gcp_set_membership": [vp, C.c_int],
@@ -319,6 +321,17 @@ class Context:
         f, m = C.c_int(), C.c_int()
         _chk(lib.gcp_dist_features(self.h, C.byref(f), C.byref(m)), "gcp_dist_features")
         return dict(fused=bool(f.value), multimem=bool(m.value))
+
+    def layout(self):
+        a, o, f = C.c_int(), C.c_int(), C.c_int()
+        _chk(lib.gcp_layout(self.h, C.byref(a), C.byref(o), C.byref(f)), "gcp_layout")
+        return dict(ag_interleaved=bool(a.value), slot_order=bool(o.value), filter=bool(f.value))
+
+    def debug_nonzero_j(self, seed, rank, it, N, first, count):
+        out = np.zeros(count, np.int64)
+        _chk(lib.gcp_debug_nonzero_j(self.h, seed, rank, it, N, first, count, _ptr(out, C.c_int64)),
+             "gcp_debug_nonzero_j")
+        return out
 
     def profile_enable(self, on=True):
         _chk(lib.gcp_profile_enable(self.h, int(on)), "gcp_profile_enable")

@@ -26,7 +26,14 @@ def main():
     if mode == "sync32":
         os.environ["GCP_MULTIMEM"] = "1"   # exercise the NVLS path whatever P is
     mode = "sync" if mode == "sync32" else mode
-    TG, TM, TE = (1e-4, 1e-3, 1e-4) if prec == "fp32" else (1e-10, 1e-9, 1e-10)
+    # TG, TE: the C18 bounds (gradient per element vs the rounding scale S, loss
+    # estimate vs sum |terms|) from an identical state.  TM / TM_FIT / TE_FIT bound
+    # multi-step trajectories (5 iterations; a 3-epoch fit of 18), where C18 sets
+    # no bound: DESIGN.md §5.3 derives them from Adam's sensitivity
+    # |d(B^/sqrt(C^+eps))/dg| <= 1/sqrt(eps) applied to the per-step rounding
+    # difference of the gradient, summed over the steps.
+    TG, TE = (1e-4, 1e-4) if prec == "fp32" else (1e-10, 1e-10)
+    TM, TM_FIT, TE_FIT = (1e-3, 1e-2, 1e-3) if prec == "fp32" else (1e-9, 1e-8, 1e-9)
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -111,10 +118,10 @@ def main():
     Af, hist, obest = oracle.fit(blocks, grid, A0, loss, iters=6, mode=omode, tau=tau, meta_rate=5e-3, **kw)
     assert len(rows) == len(hist), (rows, hist)
     for r, h in zip(rows, hist):
-        assert abs(r[2] - h[0]) <= 10 * TE * abs(h[0]), (r, h)
+        assert abs(r[2] - h[0]) <= TE_FIT * abs(h[0]), (r, h)
     for k in range(3):
         want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
-        assert np.allclose(ctx.model_get(k), want, rtol=10 * TM, atol=TM), f"fit model k={k}"
+        assert np.allclose(ctx.model_get(k), want, rtol=TM_FIT, atol=TM), f"fit model k={k}"
     # replace-ingest on the same context (a repeated job): the grid is unchanged, so
     # the slice communicators and the symmetric windows are reused, not re-created;
     # the fit must repeat the oracle's trajectory
@@ -123,10 +130,10 @@ def main():
     _, rows2 = ctx.fit(fp)
     assert len(rows2) == len(hist), (rows2, hist)
     for r, h in zip(rows2, hist):
-        assert abs(r[2] - h[0]) <= 10 * TE * abs(h[0]), ("replace-ingest", r, h)
+        assert abs(r[2] - h[0]) <= TE_FIT * abs(h[0]), ("replace-ingest", r, h)
     for k in range(3):
         want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
-        assert np.allclose(ctx.model_get(k), want, rtol=10 * TM, atol=TM), f"replace-ingest fit model k={k}"
+        assert np.allclose(ctx.model_get(k), want, rtol=TM_FIT, atol=TM), f"replace-ingest fit model k={k}"
     ctx.close()
     dist.barrier()
     if rank == 0:

@@ -117,10 +117,10 @@ def test_gradient_parity(gcp, orc, loss, strategy, prec):
     A = _model(c, 3)
     ls = c.loss_grad(loss, want_loss=True)
     G = [c.grad_get(k) for k in range(3)]
-    Go, S, lo = orc.sampled_grad(t, A, loss, 3001, 0, 0, p, q, strategy)
+    Go, S, lo, lsc = orc.sampled_grad(t, A, loss, 3001, 0, 0, p, q, strategy, loss_scale=True)
     _grad_check(G, Go, S, TOL[prec], f"{loss}/{strategy}/{prec}")
-    # sampled loss sum_s w f: relative to the sum of |w f| scales
-    assert abs(ls - lo) <= TOL[prec] * max(1.0, abs(lo)) * 10
+    # sampled loss sum_s w f: C18, |dF| <= tol * sum |terms| (rounding scales of f)
+    assert abs(ls - lo) <= TOL[prec] * lsc, (ls, lo, lsc, abs(ls - lo) / lsc)
 
 
 @pytest.mark.parametrize("interleave", ["0", "1"])
@@ -197,8 +197,10 @@ def test_adam_parity_from_identical_gradient(gcp, orc, prec):
         c.adam_step(p)
         orc.adam(A, G, B, Cm, step, 1e-2, 0.9, 0.999, 1e-8, 0.0)
         Ag = np.concatenate([a.ravel() for a in _model(c, 3)])
-        tol = TOL[prec]
-        assert np.all(np.abs(Ag - A) <= tol * np.maximum(np.abs(A), 1.0) * 10 + 1e-4 * 1e-2 * (prec == "fp32"))
+        # C18: elementwise relative tol with an absolute floor tol * alpha
+        tol, alpha = TOL[prec], 1e-2
+        err = np.abs(Ag - A)
+        assert np.all(err <= tol * np.abs(A) + tol * alpha), (step, (err / (tol * np.abs(A) + tol * alpha)).max())
         A = Ag.copy()  # continue from the GPU state (identical-state protocol, C18)
         assert (Ag >= 0).all()  # Poisson clamp l = 0
     ctr = c.counters()
@@ -404,10 +406,10 @@ def test_gradient_parity_row_geometries(gcp, orc, prec, R):
     c.loss_grad("poisson")
     G = [c.grad_get(k) for k in range(3)]
     Go, S, _ = orc.sampled_grad(t, A, "poisson", 3001, 0, 0, 600, 600)
-    _grad_check(G, Go, S, TOL[prec] * (10 if prec == "fp32" and R > 32 else 1), f"R={R}/{prec}")
+    _grad_check(G, Go, S, TOL[prec], f"R={R}/{prec}")
     est = c.loss_estimate("poisson", 1500, 1500, 4001)
     oe, scale = orc.loss_estimate(t, A, "poisson", 4001, 0, 1500, 1500)
-    assert abs(est - oe) <= TOL[prec] * scale * (10 if R > 32 else 1)
+    assert abs(est - oe) <= TOL[prec] * scale, (est, oe, abs(est - oe) / scale)
 
 
 @pytest.mark.parametrize("dims", [(60, 70), (9, 10, 11, 12), (4, 5, 6, 5, 4, 6)])
@@ -431,3 +433,63 @@ def test_gradient_parity_orders(gcp, orc, dims):
     G = [c.grad_get(k) for k in range(len(dims))]
     Go, S, _ = orc.sampled_grad(t, A, "gaussian", 3001, 0, 0, 500, 700)
     _grad_check(G, Go, S, TOL["fp64"], f"d={len(dims)}")
+
+
+def test_slot_order_survives_model_reinit(gcp, orc, monkeypatch):
+    """Regression (round-1 advisor, high): with the slot order on, a model
+    re-initialised at another R (another K2 geometry and partial count) keeps
+    valid order buffers: the gradient after model_init(16) -> loss_grad ->
+    model_init(4) -> loss_grad still matches the oracle."""
+    monkeypatch.setenv("GCP_SLOT_ORDER", "1")
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = gcp.Context(0, None, "fp32")
+    c.tensor_create(dims, subs, vals)
+    t = orc.Tensor(dims, subs, vals)
+    for R in (16, 4, 16, 2):
+        c.model_init(R, 2001)
+        assert c.layout()["slot_order"]
+        c.sample("stratified", 1500, 1700, 3001)
+        A = _model(c, 3)
+        c.loss_grad("poisson")
+        G = [c.grad_get(k) for k in range(3)]
+        Go, S, _ = orc.sampled_grad(t, A, "poisson", 3001, 0, 0, 1500, 1700)
+        _grad_check(G, Go, S, TOL["fp32"], f"reinit R={R}")
+    # a replaced tensor rebuilds the per-tensor bucket table
+    subs2, vals2 = gcp_synth.chi_kolda(dims, 1800, 4, 1009, loss="poisson")
+    subs2, vals2 = subs2.numpy(), vals2.numpy()
+    c.tensor_create(dims, subs2, vals2)
+    c.model_init(4, 2001)
+    t2 = orc.Tensor(dims, subs2, vals2)
+    c.sample("stratified", 900, 1100, 3001)
+    A = _model(c, 3)
+    c.loss_grad("poisson")
+    Go, S, _ = orc.sampled_grad(t2, A, "poisson", 3001, 0, 0, 900, 1100)
+    _grad_check([c.grad_get(k) for k in range(3)], Go, S, TOL["fp32"], "replaced tensor")
+
+
+def test_dims_product_overflow_is_an_error(gcp):
+    """prod I_k must fit in 128 bits: five modes of 2^32 - 1 do not."""
+    c = gcp.Context(0, None, "fp32")
+    with pytest.raises(gcp.GcpError) as e:
+        c.tensor_create((2 ** 32 - 1,) * 5, np.array([[0, 0, 0, 0, 0]]), np.array([1.0]))
+    assert e.value.name == "GCP_E_ARG"
+    c.tensor_create((2 ** 32 - 1,) * 4, np.array([[0, 0, 0, 0]]), np.array([1.0]))   # 128 bits: fine
+
+
+def test_nonzero_index_beyond_2_32(gcp, orc):
+    """Reading R11 index map j = floor(W0 N / 2^64) on the device draw path for
+    N >= 2^32 (c5 holds 4.69e9 nonzeros; the kernel keeps 32 bits of j in flight
+    and re-derives the full j): bit-exact against Philox + Python integers."""
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals)
+    seed = (11 << 32) | 3005
+    for N, rank, it in ((4_687_474_081, 0, 7), (2 ** 32, 3, 0), (2 ** 40 + 12345, 1, 123456), (2 ** 32 - 1, 0, 2)):
+        first, count = 1_000_000, 4096
+        j = c.debug_nonzero_j(seed, rank, it, N, first, count)
+        for s in range(first, first + count, 37):
+            o = orc.philox([s, rank, 0, it], [seed & 0xFFFFFFFF, seed >> 32])
+            W0 = o[0] | (o[1] << 32)
+            assert j[s - first] == (W0 * N) >> 64, (N, s)
+        assert j.max() >= 2 ** 32 or N <= 2 ** 32

@@ -195,6 +195,21 @@ def test_poisson_gradient_closed_form(orc):
         assert np.allclose(G[k], ref, rtol=1e-12, atol=1e-13)
 
 
+def test_poisson_exact_grad_at_scale_matches_enumeration(orc):
+    """oracle.poisson_exact_grad (the O(N d R) closed form used as the exact
+    target at c2 scale) equals the enumerated gradient of F."""
+    for dims, R, nnz, seed in (((6, 5, 4), 3, 30, 19), ((7, 3, 5, 4), 2, 50, 20)):
+        rng = np.random.default_rng(seed)
+        subs, vals = gcp_synth.uniform_sparse(dims, nnz, seed=seed + 1, values="counts")
+        t = orc.Tensor(dims, subs, vals)
+        A = [rng.uniform(0.1, 1, size=(I, R)) for I in dims]
+        lam = rng.uniform(0.5, 1.5, size=R)
+        G = orc.full_grad(t, A, "poisson", lam)
+        Gs = orc.poisson_exact_grad(subs, vals, A, lam, chunk=7)   # ragged chunks
+        for k in range(len(dims)):
+            assert np.allclose(Gs[k], G[k], rtol=1e-12, atol=1e-12 * np.abs(G[k]).max())
+
+
 def test_full_loss_closed_forms(orc):
     dims = (5, 4, 3)
     R = 2
