@@ -64,7 +64,8 @@ def _unlin(keys, dims):
 
 
 def _merge2(hi, lo, cnt):
-    """Merge duplicate (hi, lo) keys, summing counts; result sorted by (hi, lo)."""
+    """Merge duplicate (hi, lo) keys, summing counts; result sorted by (hi, lo).
+    Keeps the dtypes of hi and cnt (int32 in the compact billion-scale parts)."""
     o = torch.argsort(lo, stable=True)
     hi, lo, cnt = hi[o], lo[o], cnt[o]
     o = torch.argsort(hi, stable=True)
@@ -74,12 +75,12 @@ def _merge2(hi, lo, cnt):
     new[1:] = (hi[1:] != hi[:-1]) | (lo[1:] != lo[:-1])
     seg = torch.cumsum(new, 0) - 1
     cu = torch.zeros(int(seg[-1]) + 1 if seg.numel() else 0, dtype=torch.int64, device=hi.device)
-    cu.index_add_(0, seg, cnt)
-    return hi[new], lo[new], cu
+    cu.index_add_(0, seg, cnt.long())
+    return hi[new], lo[new], cu.to(cnt.dtype)
 
 
 def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, boost=10.0,
-              tol=0.005, max_rounds=64, force_wide=False, block=None, allreduce=None):
+              tol=0.005, max_rounds=64, force_wide=False, block=None, allreduce=None, out_device=None):
     """Return (subs int64 [N, d], vals float64 [N]) as torch tensors on `device`.
 
     Duplicate draws merge on an int64 mixed-radix key when prod(dims) < 2^62,
@@ -91,7 +92,15 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
     one global tensor; `allreduce(int) -> int` sums the kept distinct counts over
     the ranks, so the top-up test sees the global count.  Only the rare thinning
     step (an overshoot beyond nnz * (1 + tol)) and the shuffle order then depend
-    on the block."""
+    on the block.
+
+    out_device: where the returned tensors live (default `device`).  On the
+    billion-scale path with out_device="cpu" each finished i_1 partition moves to
+    host memory as it is built, so a tensor larger than the device's memory (c5
+    at one GPU: 4.69e9 nonzeros, 150 GB of int64 + fp64 COO) can be generated
+    on the device.  The partitions are kept compact while merging (i_1 and the
+    counts as int32), which changes no value."""
+    out_device = device if out_device is None else out_device
     dims = [int(i) for i in dims]
     wide = force_wide or block is not None or math.prod(dims) >= 2 ** 62
     assert not wide or math.prod(dims[1:]) < 2 ** 63
@@ -145,7 +154,11 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
         blo, bhi = (list(block[0]), list(block[1])) if block is not None else ([0] * len(dims), dims)
         nparts = max(1, -(-nnz // 200_000_000))
         edges = [int(blo[0]) + (int(bhi[0]) - int(blo[0])) * j // nparts for j in range(nparts + 1)]
-        parts = [(torch.empty(0, dtype=torch.int64, device=device),) * 3 for _ in range(nparts)]
+        # compact partitions: i_1 (< 2^31) and the counts as int32, the key of the
+        # other modes as int64 (16 B per distinct entry while merging)
+        assert dims[0] < 2 ** 31
+        parts = [(torch.empty(0, dtype=torch.int32, device=device), torch.empty(0, dtype=torch.int64, device=device),
+                  torch.empty(0, dtype=torch.int32, device=device)) for _ in range(nparts)]
         total = 0
         for _ in range(max_rounds):
             left = max(1024, int((nnz - total) * 1.02) + 64)
@@ -168,8 +181,8 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
                 for j in range(nparts):
                     m = pid == j
                     ph, pl, pc = parts[j]
-                    parts[j] = _merge2(torch.cat([ph, nhi[m]]), torch.cat([pl, nlo[m]]),
-                                       torch.cat([pc, torch.ones(int(m.sum()), dtype=torch.int64, device=device)]))
+                    parts[j] = _merge2(torch.cat([ph, nhi[m].int()]), torch.cat([pl, nlo[m]]),
+                                       torch.cat([pc, torch.ones(int(m.sum()), dtype=torch.int32, device=device)]))
                 del nhi, nlo, pid
             total = sum(p[0].numel() for p in parts)
             if allreduce is not None:
@@ -178,6 +191,12 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
                 break
         keep = nnz / total if total > nnz * (1 + tol) else None
         subs_l, cnt_l = [], []
+        to_host = torch.device(out_device) != torch.device(device)
+        if to_host:   # filled partition by partition; capacity bound: the tolerance band
+            cap = int(nnz * (1 + tol)) + 1_000_000
+            subs = torch.empty((cap, len(dims)), dtype=torch.int64, device=out_device)
+            counts = torch.empty(cap, dtype=torch.float64, device=out_device)   # the values, filled directly
+            o = 0
         for j in range(nparts):
             ph, pl, pc = parts[j]
             parts[j] = None
@@ -189,17 +208,30 @@ def chi_kolda(dims, nnz, R, seed, loss="poisson", device="cpu", boost_frac=0.1, 
             sj = torch.empty((ph.numel(), len(dims)), dtype=torch.int64, device=device)
             sj[:, 0] = ph
             sj[:, 1:] = _unlin(pl, dims[1:])
-            subs_l.append(sj)
-            cnt_l.append(pc)
-            del ph, pl, perm
-        subs = torch.cat(subs_l)
-        del subs_l
-        counts = torch.cat(cnt_l)
-        del cnt_l
-    if loss == "bernoulli":
-        vals = torch.ones(counts.numel(), dtype=torch.float64, device=device)
+            if to_host:
+                n = sj.shape[0]
+                assert o + n <= cap
+                subs[o:o + n] = sj
+                counts[o:o + n] = pc.double() if loss != "bernoulli" else 1.0
+                o += n
+            else:
+                subs_l.append(sj)
+                cnt_l.append(pc.long())
+            del ph, pl, perm, sj
+        if to_host:
+            subs, counts = subs[:o], counts[:o]
+        else:
+            subs = torch.cat(subs_l)
+            counts = torch.cat(cnt_l)
+        del subs_l, cnt_l
+    if counts.dtype == torch.float64:   # host-assembled billion-scale values (already final)
+        vals = counts
+    elif loss == "bernoulli":
+        vals = torch.ones(counts.numel(), dtype=torch.float64, device=counts.device)
     else:
         vals = counts.double()
+    if not wide and torch.device(out_device) != torch.device(device):
+        subs, vals = subs.to(out_device), vals.to(out_device)
     return subs, vals
 
 

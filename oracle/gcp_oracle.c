@@ -668,3 +668,129 @@ double orc_grid_plan(int P, int d, const int64_t *dims, int *grid_out)
     grid_rec(P, d, dims, 0, P, cur, grid_out, &best);
     return best;
 }
+
+/* ------------------------------------------------------------------------ */
+/* OpenMP timing variants (built with -fopenmp).  Same    */
+/* estimator and the same draws as orc_sampled_grad / orc_loss_estimate /      */
+/* orc_adam: the slots of each stratum split into nthreads contiguous ranges,   */
+/* thread-private G and sums, reduced in thread order.  Used only to time the   */
+/* CPU baseline on all host cores; pinned to the serial functions (fixed        */
+/* summation order aside) in tests/test_oracle_estimators.py.                  */
+/* ------------------------------------------------------------------------ */
+static int grad_range(const orc_tensor *t, const orc_model *m, int loss, int strategy, uint64_t seed,
+                      uint32_t rank, uint32_t it, double w_nz, double w_z, int64_t nz0, int64_t nz1,
+                      int64_t z0, int64_t z1, double *G_flat, double *lsum)
+{
+    int d = t->d;
+    int64_t coords[32];
+    for (int64_t s = nz0; s < nz1; ++s) {
+        int64_t j = draw_nonzero(t, seed, rank, KIND_GRAD_NZ, it, (uint32_t)s);
+        memcpy(coords, t->subs + j * d, sizeof(int64_t) * d);
+        double x = t->vals[j];
+        double mv = model_value(m, t, coords);
+        mttkrp_entry(m, t, coords, sample_y(loss, strategy, 1, w_nz, x, mv), G_flat, 0.0, NULL);
+        *lsum += w_nz * orc_loss_f(loss, x, mv);
+    }
+    for (int64_t s = z0; s < z1; ++s) {
+        if (draw_zero(t, seed, rank, KIND_GRAD_Z, it, (uint32_t)s, strategy == ORC_STRATIFIED, coords) < 0)
+            return ORC_E_REJECT_CAP;
+        double mv = model_value(m, t, coords);
+        mttkrp_entry(m, t, coords, sample_y(loss, strategy, 0, w_z, 0.0, mv), G_flat, 0.0, NULL);
+        *lsum += w_z * orc_loss_f(loss, 0.0, mv);
+    }
+    return ORC_OK;
+}
+
+static int64_t coef_count(const orc_tensor *t, int R)
+{
+    int64_t n = 0;
+    for (int k = 0; k < t->d; ++k) n += (t->hi[k] - t->lo[k]) * (int64_t)R;
+    return n;
+}
+
+int orc_sampled_grad_par(const orc_tensor *t, int R, const double *lambda, const double *A_flat,
+                         int loss, int strategy, uint64_t seed, uint32_t rank, uint32_t it,
+                         int64_t p_w, int64_t q_w, double *G_flat, double *loss_out, int nthreads)
+{
+    orc_model m; make_model(&m, t, R, lambda, A_flat);
+    if (p_w > 0 && t->N == 0) return ORC_E_NO_NONZEROS;
+    if (q_w > 0 && strategy == ORC_STRATIFIED && block_M(t) == (u128)t->N) return ORC_E_NO_ZEROS;
+    if (nthreads < 1) nthreads = 1;
+    double w_nz = p_w > 0 ? weight_nz(t, p_w) : 0.0;
+    double w_z = q_w > 0 ? weight_z(t, q_w) : 0.0;
+    int64_t nc = coef_count(t, R);
+    double *priv = calloc((size_t)nthreads * (size_t)nc, sizeof(double));
+    double *ls = calloc((size_t)nthreads, sizeof(double));
+    int *st = calloc((size_t)nthreads, sizeof(int));
+    if (!priv || !ls || !st) { free(priv); free(ls); free(st); return ORC_E_OOM; }
+#pragma omp parallel for num_threads(nthreads) schedule(static, 1)
+    for (int w = 0; w < nthreads; ++w)
+        st[w] = grad_range(t, &m, loss, strategy, seed, rank, it, w_nz, w_z,
+                           p_w * w / nthreads, p_w * (w + 1) / nthreads,
+                           q_w * w / nthreads, q_w * (w + 1) / nthreads, priv + (size_t)w * nc, &ls[w]);
+    int rc = ORC_OK;
+    double lsum = 0.0;
+    for (int w = 0; w < nthreads; ++w) {
+        if (st[w]) rc = st[w];
+        lsum += ls[w];
+    }
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+    for (int64_t e = 0; e < nc; ++e) {
+        double a = G_flat[e];
+        for (int w = 0; w < nthreads; ++w) a += priv[(size_t)w * nc + e];   /* fixed thread order */
+        G_flat[e] = a;
+    }
+    if (loss_out) *loss_out = lsum;
+    free(priv); free(ls); free(st);
+    return rc;
+}
+
+int orc_loss_estimate_par(const orc_tensor *t, int R, const double *lambda, const double *A_flat,
+                          int loss, uint64_t seed, uint32_t rank, int64_t f_nz, int64_t f_z,
+                          double *est_out, int nthreads)
+{
+    orc_model m; make_model(&m, t, R, lambda, A_flat);
+    const uint32_t it = 0xFFFFFFFFu;
+    if (f_nz > 0 && t->N == 0) return ORC_E_NO_NONZEROS;
+    if (f_z > 0 && block_M(t) == (u128)t->N) return ORC_E_NO_ZEROS;
+    if (nthreads < 1) nthreads = 1;
+    double w_nz = f_nz > 0 ? weight_nz(t, f_nz) : 0.0;
+    double w_z = f_z > 0 ? weight_z(t, f_z) : 0.0;
+    double *snz = calloc((size_t)nthreads, sizeof(double)), *sz = calloc((size_t)nthreads, sizeof(double));
+    int *st = calloc((size_t)nthreads, sizeof(int));
+    if (!snz || !sz || !st) { free(snz); free(sz); free(st); return ORC_E_OOM; }
+#pragma omp parallel for num_threads(nthreads) schedule(static, 1)
+    for (int w = 0; w < nthreads; ++w) {
+        int64_t coords[32];
+        for (int64_t s = f_nz * w / nthreads; s < f_nz * (w + 1) / nthreads; ++s) {
+            int64_t j = draw_nonzero(t, seed, rank, KIND_F_NZ, it, (uint32_t)s);
+            memcpy(coords, t->subs + j * t->d, sizeof(int64_t) * t->d);
+            snz[w] += orc_loss_f(loss, t->vals[j], model_value(&m, t, coords));
+        }
+        for (int64_t s = f_z * w / nthreads; s < f_z * (w + 1) / nthreads; ++s) {
+            if (draw_zero(t, seed, rank, KIND_F_Z, it, (uint32_t)s, 1, coords) < 0) { st[w] = ORC_E_REJECT_CAP; break; }
+            sz[w] += orc_loss_f(loss, 0.0, model_value(&m, t, coords));
+        }
+    }
+    double a = 0.0, b = 0.0;
+    int rc = ORC_OK;
+    for (int w = 0; w < nthreads; ++w) { a += snz[w]; b += sz[w]; if (st[w]) rc = st[w]; }
+    *est_out = w_nz * a + w_z * b;
+    free(snz); free(sz); free(st);
+    return rc;
+}
+
+void orc_adam_par(int64_t n, double *A, const double *G, double *B, double *C, int64_t t,
+                  double alpha, double beta1, double beta2, double eps, double lower, int nthreads)
+{
+    double bc1 = 1.0 - pow(beta1, (double)t);
+    double bc2 = 1.0 - pow(beta2, (double)t);
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        B[i] = beta1 * B[i] + (1.0 - beta1) * G[i];
+        C[i] = beta2 * C[i] + (1.0 - beta2) * G[i] * G[i];
+        double a = A[i] - alpha * ((B[i] / bc1) / sqrt(C[i] / bc2 + eps));
+        A[i] = a < lower ? lower : a;
+    }
+}

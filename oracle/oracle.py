@@ -41,7 +41,7 @@ def build(force: bool = False) -> Path:
     """Compile gcp_oracle.c (plain -O2, no fast-math)."""
     if force or not _LIB.exists() or _LIB.stat().st_mtime < _SRC.stat().st_mtime:
         tmp = _LIB.with_suffix(f".{os.getpid()}.tmp")
-        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared",
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-fopenmp",
                                "-fno-fast-math", "-o", str(tmp), str(_SRC), "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
@@ -88,6 +88,12 @@ def lib():
                                        C.c_uint32, C.c_int64, C.c_int64, dp, dp, dp, dp, i64p]
         L.orc_loss_estimate.argtypes = [vp, C.c_int, dp, dp, C.c_int, C.c_uint64, C.c_uint32,
                                         C.c_int64, C.c_int64, dp, dp, i64p]
+        L.orc_sampled_grad_par.argtypes = [vp, C.c_int, dp, dp, C.c_int, C.c_int, C.c_uint64, C.c_uint32,
+                                           C.c_uint32, C.c_int64, C.c_int64, dp, dp, C.c_int]
+        L.orc_loss_estimate_par.argtypes = [vp, C.c_int, dp, dp, C.c_int, C.c_uint64, C.c_uint32,
+                                            C.c_int64, C.c_int64, dp, C.c_int]
+        L.orc_adam_par.argtypes = [C.c_int64, dp, dp, dp, dp, C.c_int64, C.c_double, C.c_double,
+                                   C.c_double, C.c_double, C.c_double, C.c_int]
         L.orc_full_loss.argtypes = [vp, C.c_int, dp, dp, C.c_int, dp]
         L.orc_full_grad.argtypes = [vp, C.c_int, dp, dp, C.c_int, dp]
         L.orc_adam.argtypes = [C.c_int64, dp, dp, dp, dp, C.c_int64, C.c_double, C.c_double,
@@ -338,6 +344,44 @@ def full_grad(t, A, loss, lam=None):
     _check(lib().orc_full_grad(t._h, R, _p(la, C.c_double), _p(Af, C.c_double), LOSSES[loss],
                                _p(G, C.c_double)), "full_grad guard")
     return t.split_rows(G, R)
+
+
+# ---------------------------------------------------------------- OpenMP timing variants
+def host_threads():
+    """Host threads this process may use (the CPU-baseline core count)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def sampled_grad_par(t, A, loss, seed, rank, it, p_w, q_w, strategy="stratified", lam=None, nthreads=None):
+    """OpenMP variant of sampled_grad (timing only): same
+    draws, thread-private G reduced in thread order.  Returns (G, sampled loss)."""
+    R = A[0].shape[1]
+    Af, la = _f64(t.block_rows(A)), _lam(lam, R)
+    G = np.zeros_like(Af)
+    ls = C.c_double(0)
+    st = lib().orc_sampled_grad_par(t._h, R, _p(la, C.c_double), _p(Af, C.c_double), LOSSES[loss],
+                                    STRATEGIES[strategy], seed, rank, it, p_w, q_w, _p(G, C.c_double),
+                                    C.byref(ls), nthreads or host_threads())
+    _check(st)
+    return t.split_rows(G, R), ls.value
+
+
+def loss_estimate_par(t, A, loss, seed, rank, f_nz, f_z, lam=None, nthreads=None):
+    R = A[0].shape[1]
+    Af, la = _f64(t.block_rows(A)), _lam(lam, R)
+    est = C.c_double(0)
+    st = lib().orc_loss_estimate_par(t._h, R, _p(la, C.c_double), _p(Af, C.c_double), LOSSES[loss],
+                                     seed, rank, f_nz, f_z, C.byref(est), nthreads or host_threads())
+    _check(st)
+    return est.value
+
+
+def adam_par(A, G, B, Cm, t, alpha, beta1=0.9, beta2=0.999, eps=1e-8, lower=-math.inf, nthreads=None):
+    lib().orc_adam_par(A.size, _p(A, C.c_double), _p(G, C.c_double), _p(B, C.c_double),
+                       _p(Cm, C.c_double), t, alpha, beta1, beta2, eps, lower, nthreads or host_threads())
 
 
 def poisson_exact_grad(subs, vals, A, lam=None, chunk=4_000_000):

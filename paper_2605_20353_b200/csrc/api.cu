@@ -207,12 +207,15 @@ ModelArgs model_args(const gcp_ctx* c) {
 // the slot-order buffers (their table T is per tensor: dropped with the tensor)
 void ord_free(gcp_ctx* c) {
     graph_drop(c);
+    c->ord_hist_ready = false;
     gfree(c, c->d_ord_buf);
     c->d_ord_buf = nullptr;
     c->d_ord_T = nullptr;
+    c->d_ord_lut = nullptr;
     c->d_ord_cnt = nullptr;
     c->d_ord = nullptr;
     c->d_ord_key = nullptr;
+    c->d_ord_rank = nullptr;
     c->ord_cap = 0;
 }
 
@@ -706,6 +709,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     c->t = 0;
     c->ts = 0;
     c->it = 0;
+    c->ord_hist_ready = false;
     c->grad_blocks = sample_kernel_blocks(c);
     ST_TRY(ensure_partials(c, c->grad_blocks));
     c->have_model = true;
@@ -792,6 +796,7 @@ gcp_status gcp_sample(gcp_ctx* c, gcp_strategy strategy, int64_t s_nz, int64_t s
     c->q_w = q_w;
     c->seed = seed;
     c->bound = true;
+    c->ord_hist_ready = false;
     graph_drop(c);
     return GCP_OK;
 }
@@ -874,10 +879,13 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
             }
         }
         if (c->slot_order && n_slots <= c->ord_cap) {
+            // the histogram pass may have run inside the previous Adam launch
+            const bool done = c->ord_hist_ready && c->ord_hist_it == c->it;
             prof_begin(c, PROF_OTHER, &ev);
-            CUDA_TRY(c, launch_slot_order(c, s, &so.order), "slot order");
+            CUDA_TRY(c, launch_slot_order(c, s, &so.order, done), "slot order");
             prof_end(c, PROF_OTHER, ev);
         }
+        c->ord_hist_ready = false;
     }
     prof_begin(c, PROF_GRAD, &ev);
     CUDA_TRY(c, launch_sample_kernel(c, so, m, loss, 0, !stratified, weight_nz(c, c->p_w), weight_z(c, c->q_w),
@@ -944,13 +952,26 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
         seg.len[0] = c->n_coef;
         seg.n = 1;
     }
+    // the next iteration's slot-order histogram rides along in this (memory-bound) launch
+    OrdHistArgs oh;
+    oh.n = 0;
+    bool fused_hist = false;
+    if (c->slot_order && !two_sided(c) && c->bound && c->ord_cap > 0) {
+        int64_t vecs = 0;
+        for (int i = 0; i < seg.n; ++i) vecs += seg.len[i] / (c->prec == GCP_FP32 ? 4 : 2);
+        const SampleArgs nx = sample_args(c, c->p_w, c->q_w, c->seed, c->it + 1, KIND_GRAD_NZ, KIND_GRAD_Z,
+                                          c->strategy == GCP_STRATIFIED);
+        fused_hist = ord_hist_args(c, nx, &oh, vecs);
+    }
     cudaEvent_t ev;
     prof_begin(c, PROF_ADAM, &ev);
     CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower,
                             c->capturing ? c->t - c->graph_t0 : c->t, sharded ? 0 : 1, c->ag_stride,
-                            c->capturing ? c->d_step : nullptr),
+                            c->capturing ? c->d_step : nullptr, fused_hist ? &oh : nullptr),
              "gcp_adam_step");
     prof_end(c, PROF_ADAM, ev);
+    c->ord_hist_ready = fused_hist;
+    c->ord_hist_it = c->it + 1;
     if (sharded) {
         CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, (size_t)c->n_coef * tsz(c), c->stream), "adam G reset");
         if (!two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // two-sided: rows stay partitioned

@@ -76,6 +76,20 @@ struct ModelArgs {
     int row_stride;           // elements between consecutive rows (R_pad, or 2 R_pad when A/G interleave)
 };
 
+// The slot-order histogram pass of the NEXT iteration, fused into the Adam
+// kernel of this one (kernels.cu, launch_slot_order): n = 0 means none.
+struct OrdHistArgs {
+    SampleArgs sa;            // the next iteration's sampler arguments
+    const uint16_t* lut;      // per-tensor lookup: bucket of nonzero index j = lut[j >> lut_shift]
+    int lut_shift;
+    uint16_t* keys;           // bucket per slot (out)
+    uint32_t* ranks;          // rank of the slot inside its bucket (out)
+    uint32_t* totals;         // bucket totals (global atomicAdd)
+    int bits;                 // log2 bucket count
+    int ratio;                // one slot per `ratio` Adam vectors of a thread
+    int64_t n;                // slots (p + q)
+};
+
 struct Segment {              // contiguous ranges of the coefficient arrays (Adam)
     int64_t start[2 * kMaxModes];
     int64_t len[2 * kMaxModes];
@@ -144,6 +158,7 @@ struct gcp_ctx {
     uint64_t* d_filter = nullptr;              // L2-resident negative test in front of the zero test
     cudaMemPool_t scratch_pool = nullptr;      // ingest scratch (ingest.cu)
     uint64_t filter_sectors = 0;
+    bool lean_ingest = false;                  // the last ingest took the lean (key, value) sort path
     // ---- model
     bool have_model = false;
     int R = 0, R_pad = 0;
@@ -178,11 +193,17 @@ struct gcp_ctx {
     // slot ordering (kernels.cu launch_slot_order): the gradient K2 visits its slots
     // grouped by mode-1 position; one allocation (d_ord_buf) sized for ord_cap slots
     void* d_ord_buf = nullptr;
-    int64_t* d_ord_T = nullptr;         // per-tensor bucket -> first record table (kOrdB + 1)
+    int64_t* d_ord_T = nullptr;         // per-tensor bucket -> first record table (2^bits + 1)
+    uint16_t* d_ord_lut = nullptr;      // per-tensor nonzero index -> bucket lookup (kernels.cu)
+    int ord_lut_shift = 0;
     uint32_t* d_ord_cnt = nullptr;      // bucket totals, cursors
     uint32_t* d_ord = nullptr;          // visiting order (slot ids)
     uint16_t* d_ord_key = nullptr;      // bucket per slot
+    uint32_t* d_ord_rank = nullptr;     // rank of the slot inside its bucket
     int64_t ord_cap = 0;
+    int ord_bits = 15;                  // log2 of the bucket count (GCP_ORD_BITS)
+    bool ord_hist_ready = false;        // the histogram pass of iteration ord_hist_it ran inside an Adam launch
+    uint32_t ord_hist_it = 0;
     int slot_order = 0;                 // decided in gcp_model_init (GCP_SLOT_ORDER overrides)
     cudaGraphExec_t graph_exec = nullptr;
     double graph_key[8] = {0};
@@ -232,14 +253,16 @@ cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArg
                                  double* partials, int nblocks);
 size_t slot_order_bytes(int64_t cap);
 cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap);   // carve buffers, build the per-tensor table
-cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out);
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, bool hist_done);
+bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh, int64_t adam_vecs);
 cudaError_t launch_reduce_partials(gcp_ctx* c, const double* partials, int n, double* out);
 cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C,
                         double rate, double beta1, double beta2, double eps, double lower,
                         int64_t t, int zero_g, int row_stride = 0,    // row_stride 0: contiguous A/G
-                        const DevStep* step = nullptr);               // step: t = step->t + t (offset), rate
+                        const DevStep* step = nullptr,                // step: t = step->t + t (offset), rate
+                        const OrdHistArgs* oh = nullptr);             // fused next-iteration slot histogram
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
 cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);

@@ -184,6 +184,71 @@ __global__ void k_contains(const KeyArgs ka, int64_t n, const int64_t* __restric
     }
 }
 
+// ---- lean path (billion-nonzero blocks, u64 keys): sort (key, value) pairs
+// directly -- no coordinate array, no permutation -- then decode the records
+// from the sorted keys (the key is the mixed-radix block index, so the local
+// coordinates are its digits).
+template <typename T>
+__global__ void k_convert_lean(const KeyArgs ka, int64_t base, int64_t n, const int64_t* __restrict__ subs,
+                               const double* __restrict__ vals, T* __restrict__ valt, uint64_t* __restrict__ keys,
+                               unsigned* flags) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = 0;
+        unsigned bad = 0;
+        for (int k = 0; k < ka.d; ++k) {
+            const int64_t i = subs[x * ka.d + k];
+            if (i < ka.lo[k] || i >= ka.hi[k]) {
+                bad |= BAD_RANGE;
+                continue;
+            }
+            key = key * ka.bdim[k] + (uint64_t)(i - ka.lo[k]);
+        }
+        const double v = vals[x];
+        if (!isfinite(v)) bad |= BAD_VALUE;
+        if (bad) atomicOr(flags, bad);
+        valt[base + x] = (T)v;
+        keys[base + x] = key;
+    }
+}
+
+template <typename T>
+__global__ void k_records_from_keys(const KeyArgs ka, int64_t n, int rec_words, const uint64_t* __restrict__ keys,
+                                    const T* __restrict__ valt, uint32_t* __restrict__ rec) {
+    constexpr int VW = (int)(sizeof(T) / 4);
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const T v = valt[x];
+        memcpy(w, &v, sizeof(T));
+        uint64_t key = keys[x];
+        for (int k = ka.d - 1; k > 0; --k) {
+            w[VW + k] = (uint32_t)(key % ka.bdim[k]);
+            key /= ka.bdim[k];
+        }
+        w[VW] = (uint32_t)key;
+        uint4* dst = reinterpret_cast<uint4*>(rec + x * rec_words);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        if (rec_words == 8) dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
+// hash set of u64 block keys recomputed from the records (the key array is
+// already freed on the lean path)
+__global__ void k_hash_insert_rec(const KeyArgs ka, int64_t n, int rec_words, int val_words,
+                                  const uint32_t* __restrict__ rec, uint64_t* h, uint64_t mask) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t* r = rec + x * rec_words + val_words;
+        uint64_t key = r[0];
+        for (int k = 1; k < ka.d; ++k) key = key * ka.bdim[k] + r[k];
+        uint64_t s = (hash_key(key, 0) & mask) & ~3ull;
+        for (;;) {
+            const unsigned long long prev =
+                atomicCAS(reinterpret_cast<unsigned long long*>(h + s), kEmpty, (unsigned long long)key);
+            if (prev == kEmpty || prev == key) break;
+            s = (s + 1) & mask;
+        }
+    }
+}
+
 static KeyArgs key_args(const gcp_ctx* c) {
     KeyArgs ka;
     ka.d = c->d;
@@ -445,12 +510,185 @@ cleanup:
     c->val_words = (int)(sizeof(T) / 4);
     c->rec_words = rec_words;
     c->hash_slots = slots;
+    c->lean_ingest = false;
+    return GCP_OK;
+}
+
+// Lean ingest (row a0 for billion-nonzero blocks, e.g. c5's 4.69e9 nonzeros at
+// one GPU): peak = 2 x (8 + sizeof(T)) B per nonzero during the sort, then
+// records (16 B) + sorted keys + values; the hash set is built from the
+// records after the keys and values are freed.  Same records, same keys, same
+// membership answers as the standard path.
+template <typename T>
+static gcp_status ingest_lean(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h,
+                              const double* vals_h) {
+    const KeyArgs ka = key_args(g);
+    const int d = g->d;
+    cudaStream_t st = c->stream;
+    cudaError_t err = cudaSuccess;
+    gcp_status status = GCP_OK;
+    const int kbits = std::max(bits_for(g->M > 0 ? g->M : 1), 1);
+    const bool sorted_member = c->member == GCP_MEMBER_SORTED;
+    const int rec_words = ((int)(sizeof(T) / 4) + d <= 4) ? 4 : 8;
+    const int nb = (int)std::min<int64_t>(std::max<int64_t>((nnz + 255) / 256, 1), (int64_t)c->sm_count * 16);
+    const int64_t chunk = std::min<int64_t>(nnz, (int64_t)1 << 26);
+    unsigned flags = 0;
+    unsigned* d_flags = nullptr;
+    int64_t* d_sc = nullptr;
+    double* d_vc = nullptr;
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    T *v0 = nullptr, *v1 = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    uint64_t* skeys = nullptr;   // sorted keys (k0 or k1)
+    T* svals = nullptr;
+    uint32_t* new_rec = nullptr;
+    uint64_t* new_hash = nullptr;
+    uint64_t* new_keys = nullptr;
+    uint64_t* new_filter = nullptr;
+    uint64_t slots = 4;
+    const uint64_t fsect = filter_sectors_for(c, nnz, sorted_member ? 4 : 12);
+
+    CK(smalloc(c, &d_flags, sizeof(unsigned)));
+    CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
+    // 1) stream the host COO through the staging buffer: keys + values
+    CK(gmalloc(c, &k0, (size_t)nnz * 8));
+    CK(smalloc(c, &v0, (size_t)nnz * sizeof(T)));
+    CK(smalloc(c, &d_sc, (size_t)chunk * d * 8));
+    CK(smalloc(c, &d_vc, (size_t)chunk * 8));
+    for (int64_t b = 0; b < nnz; b += chunk) {
+        const int64_t n = std::min(chunk, nnz - b);
+        CK(cudaMemcpyAsync(d_sc, subs_h + b * d, (size_t)n * d * 8, cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(d_vc, vals_h + b, (size_t)n * 8, cudaMemcpyDefault, st));
+        k_convert_lean<T><<<nb, 256, 0, st>>>(ka, b, n, d_sc, d_vc, v0, k0, d_flags);
+        CK(cudaGetLastError());
+        c->launches++;
+    }
+    CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    sfree(c, d_sc); d_sc = nullptr;
+    sfree(c, d_vc); d_vc = nullptr;
+    if (flags & BAD_RANGE) { status = set_error(GCP_E_RANGE, "gcp_tensor_create: coordinate outside dims / block"); goto cleanup; }
+    if (flags & BAD_VALUE) { status = set_error(GCP_E_ARG, "gcp_tensor_create: non-finite value"); goto cleanup; }
+    // 2) radix sort of (key, value) pairs over the key's bits (64-bit item count)
+    CK(gmalloc(c, &k1, (size_t)nnz * 8));
+    CK(smalloc(c, &v1, (size_t)nnz * sizeof(T)));
+    {
+        cub::DoubleBuffer<uint64_t> keys(k0, k1);
+        cub::DoubleBuffer<T> vs(v0, v1);
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, vs, nnz, 0, kbits, st));
+        CK(smalloc(c, &tmp, tmp_bytes));
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, vs, nnz, 0, kbits, st));
+        skeys = keys.Current();
+        svals = vs.Current();
+    }
+    sfree(c, tmp); tmp = nullptr;
+    if (skeys == k0) { gfree(c, k1); k1 = nullptr; } else { gfree(c, k0); k0 = nullptr; }
+    if (svals == v0) { sfree(c, v1); v1 = nullptr; } else { sfree(c, v0); v0 = nullptr; }
+    // 3) duplicates, records decoded from the keys
+    k_dupcheck<<<nb, 256, 0, st>>>(nnz, skeys, nullptr, d_flags);
+    CK(cudaGetLastError());
+    c->launches++;
+    CK(gmalloc(c, &new_rec, (size_t)nnz * rec_words * 4));
+    k_records_from_keys<T><<<nb, 256, 0, st>>>(ka, nnz, rec_words, skeys, svals, new_rec);
+    CK(cudaGetLastError());
+    c->launches++;
+    CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (flags & BAD_DUP) { status = set_error(GCP_E_DUP, "gcp_tensor_create: duplicate coordinates"); goto cleanup; }
+    sfree(c, svals);
+    v0 = v1 = nullptr;
+    // 4) zero-test structure: the sorted keys themselves (row f4), or a hash set
+    //    built from the records once the keys are gone
+    if (fsect) {
+        CK(gmalloc(c, &new_filter, (size_t)fsect * 32));
+        CK(cudaMemsetAsync(new_filter, 0, (size_t)fsect * 32, st));
+        k_filter_insert<<<nb, 256, 0, st>>>(nnz, skeys, nullptr, (unsigned long long*)new_filter, fsect - 1);
+        CK(cudaGetLastError());
+        c->launches++;
+    }
+    if (sorted_member) {
+        new_keys = skeys;
+        k0 = k1 = nullptr;
+        CK(gmalloc(c, &new_hash, 32));
+        CK(cudaMemsetAsync(new_hash, 0xFF, 32, st));
+    } else {
+        gfree(c, skeys);
+        k0 = k1 = nullptr;
+        CK(cudaStreamSynchronize(st));
+        cudaMemPoolTrimTo(c->scratch_pool, 0);
+        {
+            const uint64_t need = (uint64_t)std::ceil((double)nnz / kHashLoad);
+            while (slots < need) slots <<= 1;
+            // memory-tight blocks take a fuller table (load <= 0.75): keep 10% of
+            // the device (>= 16 GB) free for the model
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            const double reserve = std::max(16.0 * (1 << 30), 0.1 * (double)tot);
+            while ((double)slots * 8 > (double)fr - reserve && (double)nnz / (double)(slots / 2) <= 0.75)
+                slots >>= 1;
+        }
+        CK(gmalloc(c, &new_hash, (size_t)slots * 8));
+        CK(cudaMemsetAsync(new_hash, 0xFF, (size_t)slots * 8, st));
+        k_hash_insert_rec<<<nb, 256, 0, st>>>(ka, nnz, rec_words, (int)(sizeof(T) / 4), new_rec, new_hash, slots - 1);
+        CK(cudaGetLastError());
+        c->launches++;
+        CK(gmalloc(c, &new_keys, 8));
+    }
+    CK(cudaStreamSynchronize(st));
+
+cleanup:
+    sfree(c, d_flags); sfree(c, d_sc); sfree(c, d_vc); sfree(c, tmp);
+    sfree(c, v0); sfree(c, v1);
+    gfree(c, k0); gfree(c, k1);
+    if (err != cudaSuccess || status != GCP_OK) {
+        gfree(c, new_rec);
+        gfree(c, new_hash);
+        gfree(c, new_keys);
+        gfree(c, new_filter);
+        if (err == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            return set_error(GCP_E_OOM, "gcp_tensor_create: out of device memory (lean ingest)");
+        }
+        if (err != cudaSuccess) return cuda_fail(c, err, "gcp_tensor_create");
+        return status;
+    }
+    gfree(c, c->d_rec);
+    gfree(c, c->d_hash);
+    gfree(c, c->d_keys);
+    gfree(c, c->d_filter);
+    c->d_filter = new_filter;
+    c->filter_sectors = new_filter ? fsect : 0;
+    c->d_rec = new_rec;
+    c->d_hash = new_hash;
+    c->d_keys = new_keys;
+    c->key128 = 0;
+    c->val_words = (int)(sizeof(T) / 4);
+    c->rec_words = rec_words;
+    c->hash_slots = sorted_member ? 4 : slots;
+    c->lean_ingest = true;
     return GCP_OK;
 }
 
 gcp_status ingest(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const int64_t* subs_h, const double* vals_h) {
     const bool p32 = nnz < ((int64_t)1 << 32);
     gcp_status st;
+    // the lean path (u64 keys only): when the standard path's scratch (coords,
+    // values, keys and permutations, double-buffered) would not fit, or forced
+    // by GCP_INGEST=lean (tests); GCP_INGEST=standard forces the other
+    const char* env = getenv("GCP_INGEST");
+    const std::string mode = env ? env : "auto";
+    const bool k64 = bits_for(g->M > 0 ? g->M : 1) <= 64;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const double std_bytes = (double)nnz * (g->d * 4 + c->tsize + 16 + 2 * (p32 ? 4 : 8) + c->tsize * 4);
+    const bool lean = k64 && nnz > 0 && (mode == "lean" || (mode != "standard" && std_bytes > 0.8 * (double)fr));
+    if (lean) {
+        st = c->prec == GCP_FP32 ? ingest_lean<float>(c, g, nnz, subs_h, vals_h)
+                                 : ingest_lean<double>(c, g, nnz, subs_h, vals_h);
+        scratch_trim_if_tight(c);
+        return st;
+    }
     if (c->prec == GCP_FP32)
         st = p32 ? ingest_impl<float, uint32_t>(c, g, nnz, subs_h, vals_h)
                  : ingest_impl<float, uint64_t>(c, g, nnz, subs_h, vals_h);

@@ -2,6 +2,7 @@
 // helper kernels (deterministic partial-sum reduction, scale, subtract).
 #include "kernels.cuh"
 
+#include <algorithm>
 #include <string>
 
 namespace gcp {
@@ -17,9 +18,9 @@ cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int6
 cudaError_t export_f64(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
                        int32_t*);
 cudaError_t adam_f32(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int, const DevStep*);
+                     double, int64_t, int, int, int, const DevStep*, const OrdHistArgs*);
 cudaError_t adam_f64(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int, const DevStep*);
+                     double, int64_t, int, int, int, const DevStep*, const OrdHistArgs*);
 cudaError_t init_f32(gcp_ctx*, const InitArgs&, void*);
 cudaError_t init_f64(gcp_ctx*, const InitArgs&, void*);
 
@@ -45,11 +46,11 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
 
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                         double beta1, double beta2, double eps, double lower, int64_t t, int zero_g,
-                        int row_stride, const DevStep* step) {
+                        int row_stride, const DevStep* step, const OrdHistArgs* oh) {
     const int rs = row_stride > 0 ? row_stride : c->R_pad;
     return c->prec == GCP_FP32
-               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step)
-               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step);
+               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, oh)
+               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, oh);
 }
 
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
@@ -67,37 +68,43 @@ cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
 }
 
 // Slot ordering for the gradient K2 (DRAM-resident mode-1 rows: c4, c5): a
-// hand-written counting sort of the iteration's slots into kOrdB buckets of
-// mode-1 position, nonzero and zero slots interleaved (a bucket holds the
-// nonzero slots whose record lies in a mode-1 row range AND the zero slots
-// whose attempt-0 candidate lies in the same range, so K2 fills the A|G lines
-// of a row range once per iteration, not once per stratum).  The sample set,
-// and so the estimate, is unchanged; only the visiting order changes, so that
-// K2's gathers and scatter-adds of one mode-1 row meet in L2.
-//   k_ord_hist     Philox word -> bucket (nonzero: j = mulhi(W, N), then the
-//                  bucket whose record range [T[b], T[b+1]) holds j, by binary
-//                  search of the per-tensor table T in shared memory; zero:
-//                  c_1 = mulhi(W, I_1), bucket floor(c_1 B / I_1)); u16 key per
-//                  slot; shared-memory histogram; one global atomicAdd per
-//                  (CTA, bucket)
+// hand-written counting sort of the iteration's slots into 2^bits buckets of
+// mode-1 position (default 2^15), nonzero and zero slots interleaved (a bucket
+// holds the nonzero slots whose record lies in a mode-1 row range AND the zero
+// slots whose attempt-0 candidate lies in the same range, so K2 fills the A|G
+// lines of a row range once per iteration, not once per stratum).  The sample
+// set, and so the estimate, is unchanged; only the visiting order changes, so
+// that K2's gathers and scatter-adds of one mode-1 row meet in L2 and its DRAM
+// accesses walk the records and rows forward.
+//   histogram      per slot: Philox word -> bucket (kernels.cuh ord_bucket) and
+//                  the slot's rank inside its bucket (a global atomicAdd);
+//                  carried by the previous iteration's Adam launch (k_adam,
+//                  OrdHistArgs: ALU work inside a memory-bound stream), else
+//                  k_ord_hist
 //   k_ord_scan     one CTA: exclusive scan of the bucket totals -> cursors;
 //                  totals reset for the next iteration
-//   k_ord_scatter  per CTA: histogram of its keys again, one atomicAdd per
-//                  (CTA, bucket) reserves its run, slot ids scattered into it
-// Order inside a bucket is arbitrary (and run to run: CTAs reserve in arrival
-// order), which only moves the fp32 atomic summation order.
-constexpr int kOrdBits = 12;
-constexpr int kOrdB = 1 << kOrdBits;
+//   k_ord_scatter  order[cursor[bucket] + rank] = slot
+// Order inside a bucket is the atomics' arrival order (run to run it varies),
+// which only moves the fp32 atomic summation order of K2.
+constexpr int kOrdMaxBits = 15;            // table / counter capacity
 constexpr int kOrdThreads = 1024;
-constexpr size_t kOrdSmem = kOrdB * sizeof(uint32_t) + (kOrdB + 1) * sizeof(int64_t);
+constexpr int kOrdLutBits = 20;            // nonzero-index lookup cells (u16 each: 2 MB, L2-resident)
+
+// bucket bits (GCP_ORD_BITS, default 15), read once per context at allocation
+int ord_bits_env() {
+    const char* e = getenv("GCP_ORD_BITS");
+    const int b = e ? atoi(e) : 15;
+    return b < 10 ? 10 : (b > kOrdMaxBits ? kOrdMaxBits : b);
+}
 
 // T[b] = first canonical record whose c_1 >= ceil(b I_1 / B), b = 0..B (T[B] = N):
 // records are sorted with i_1 most significant (reading R15)
 __global__ void k_ord_table(const uint32_t* __restrict__ rec, int rec_words, int val_words, int64_t N, uint32_t I1,
-                            int64_t* __restrict__ T) {
+                            int bits, int64_t* __restrict__ T) {
+    const int B = 1 << bits;
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b > kOrdB) return;
-    const uint64_t row = ((uint64_t)b * I1 + kOrdB - 1) >> kOrdBits;
+    if (b > B) return;
+    const uint64_t row = ((uint64_t)b * I1 + B - 1) >> bits;
     int64_t lo = 0, hi = N;
     while (lo < hi) {
         const int64_t mid = lo + ((hi - lo) >> 1);
@@ -107,59 +114,60 @@ __global__ void k_ord_table(const uint32_t* __restrict__ rec, int rec_words, int
     T[b] = lo;
 }
 
-__global__ void __launch_bounds__(kOrdThreads) k_ord_hist(const SampleArgs a, const int64_t* __restrict__ T,
-                                                         int64_t per, uint16_t* __restrict__ keys,
-                                                         uint32_t* __restrict__ totals) {
-    extern __shared__ __align__(16) unsigned char ord_smem[];
-    int64_t* sT = reinterpret_cast<int64_t*>(ord_smem);
-    uint32_t* h = reinterpret_cast<uint32_t*>(sT + kOrdB + 1);
-    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads) h[b] = 0;
-    for (int b = threadIdx.x; b <= kOrdB; b += kOrdThreads) sT[b] = T[b];
-    __syncthreads();
-    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-    const uint32_t it = iter_word(a);
-    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, a.p + a.q);
-    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) {
-        uint32_t b;
-        if (s < a.p) {
-            const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, it, k0, k1);
-            const int64_t j = (int64_t)range_map(w.w0, (uint64_t)a.N);
-            uint32_t lo = 0, hi = kOrdB;          // largest b with T[b] <= j (T[0] = 0 <= j < T[B] = N)
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (sT[mid] <= j) lo = mid;
-                else hi = mid;
-            }
-            b = lo;
-        } else {
-            const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, it, k0, k1);
-            const uint64_t c1 = range_map(w.w0, a.bdim[0]);
-            b = (uint32_t)((c1 << kOrdBits) / a.bdim[0]);
+// lut[x] = bucket of nonzero index j = x << shift: the largest b with T[b] <= j
+__global__ void k_ord_lut(const int64_t* __restrict__ T, int bits, int shift, int64_t ncell, int64_t N,
+                          uint16_t* __restrict__ lut) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < ncell; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = min(x << shift, N - 1);
+        uint32_t lo = 0, hi = 1u << bits;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (T[mid] <= j) lo = mid;
+            else hi = mid;
         }
-        keys[s] = (uint16_t)b;
-        atomicAdd(&h[b], 1u);
+        lut[x] = (uint16_t)lo;
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads)
-        if (h[b]) atomicAdd(&totals[b], h[b]);
 }
 
-__global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__ totals, uint32_t* __restrict__ cursor) {
-    constexpr int PER = kOrdB / kOrdThreads;
-    __shared__ uint32_t wsum[kOrdThreads / 32];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    uint32_t v[PER], run = 0;
+// Histogram pass for an iteration whose histogram no Adam launch computed (the
+// first of an epoch graph, eager calls; otherwise k_adam carries it):
+// bucket and in-bucket rank of every slot, four slots per thread in flight.
+__global__ void __launch_bounds__(256) k_ord_hist(const OrdHistArgs oh) {
+    const uint32_t it = iter_word(oh.sa);
+    const uint64_t inv = oh.sa.bdim[0] > 1 ? (~0ull) / oh.sa.bdim[0] : 0;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < oh.n; s += 4 * nt) {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        v[i] = totals[t * PER + i];
-        totals[t * PER + i] = 0;
-        run += v[i];
+        for (int u = 0; u < 4; ++u)
+            if (s + u * nt < oh.n) ord_hist_slot(oh, s + u * nt, it, inv);
+    }
+}
+
+// one CTA: exclusive scan of the bucket totals -> cursors; totals reset.  The
+// totals pass through shared memory with one pad word per 32 (conflict-free
+// per-thread segments).
+__global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__ totals, uint32_t* __restrict__ cursor,
+                                                         int B) {
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    uint32_t* sv = reinterpret_cast<uint32_t*>(ord_smem);   // B + B/32 words
+    __shared__ uint32_t wsum[kOrdThreads / 32];
+    for (int i = threadIdx.x; i < B; i += kOrdThreads) {
+        sv[i + (i >> 5)] = totals[i];
+        totals[i] = 0;
+    }
+    __syncthreads();
+    const int per = B / kOrdThreads;   // B >= 2^10
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint32_t run = 0;
+    for (int i = 0; i < per; ++i) {
+        const int x = t * per + i;
+        run += sv[x + (x >> 5)];
     }
     uint32_t incl = run;   // inclusive warp scan of the per-thread sums
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
@@ -174,74 +182,121 @@ __global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__
     }
     __syncthreads();
     uint32_t base = wsum[w] + incl - run;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        cursor[t * PER + i] = base;
-        base += v[i];
+    for (int i = 0; i < per; ++i) {
+        const int x = t * per + i;
+        const uint32_t v = sv[x + (x >> 5)];
+        sv[x + (x >> 5)] = base;
+        base += v;
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < B; i += kOrdThreads) cursor[i] = sv[i + (i >> 5)];
 }
 
-__global__ void __launch_bounds__(kOrdThreads) k_ord_scatter(const uint16_t* __restrict__ keys, int64_t n,
-                                                            int64_t per, uint32_t* __restrict__ cursor,
-                                                            uint32_t* __restrict__ order) {
-    __shared__ uint32_t h[kOrdB];
-    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads) h[b] = 0;
-    __syncthreads();
-    const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(s0 + per, n);
-    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) atomicAdd(&h[keys[s]], 1u);
-    __syncthreads();
-    for (int b = threadIdx.x; b < kOrdB; b += kOrdThreads)
-        if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);   // this CTA's run of bucket b
-    __syncthreads();
-    for (int64_t s = s0 + threadIdx.x; s < s1; s += kOrdThreads) order[atomicAdd(&h[keys[s]], 1u)] = (uint32_t)s;
+// order[cursor[bucket] + rank] = slot: one pass, no atomics
+__global__ void __launch_bounds__(256) k_ord_scatter(const uint16_t* __restrict__ keys,
+                                                    const uint32_t* __restrict__ ranks, int64_t n,
+                                                    const uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += nt)
+        order[__ldg(cursor + keys[s]) + ranks[s]] = (uint32_t)s;
+}
+
+static int64_t lut_cells(int64_t N, int* shift) {
+    int sh = 0;
+    while (((N - 1) >> sh) >= ((int64_t)1 << kOrdLutBits)) ++sh;
+    *shift = sh;
+    return ((std::max<int64_t>(N, 1) - 1) >> sh) + 1;
 }
 
 size_t slot_order_bytes(int64_t cap) {
-    return (size_t)cap * (sizeof(uint32_t) + sizeof(uint16_t)) + 2 * kOrdB * sizeof(uint32_t) +
-           (kOrdB + 1) * sizeof(int64_t) + 64;
+    constexpr int B = 1 << kOrdMaxBits;
+    const size_t capr = (size_t)(cap + 15) / 16 * 16;
+    return capr * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * B * sizeof(uint32_t) + (B + 2) * sizeof(int64_t) +
+           ((size_t)1 << kOrdLutBits) * sizeof(uint16_t) + 256;
 }
 
 // Carve the order buffers out of one allocation of slot_order_bytes(cap) and
-// build the per-tensor table T (once per tensor).
+// build the per-tensor tables T and lut (once per tensor).
 cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap) {
+    constexpr int B = 1 << kOrdMaxBits;
+    const size_t capr = (size_t)(cap + 15) / 16 * 16;
+    c->ord_bits = ord_bits_env();
     char* p = static_cast<char*>(buf);
     c->d_ord_T = reinterpret_cast<int64_t*>(p);
-    p += (kOrdB + 1) * sizeof(int64_t);
+    p += (B + 2) * sizeof(int64_t);
     c->d_ord_cnt = reinterpret_cast<uint32_t*>(p);
-    p += 2 * kOrdB * sizeof(uint32_t);
+    p += 2 * B * sizeof(uint32_t);
     c->d_ord = reinterpret_cast<uint32_t*>(p);
-    p += (size_t)cap * sizeof(uint32_t);
+    p += capr * sizeof(uint32_t);
+    c->d_ord_rank = reinterpret_cast<uint32_t*>(p);
+    p += capr * sizeof(uint32_t);
     c->d_ord_key = reinterpret_cast<uint16_t*>(p);
-    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, 2 * kOrdB * sizeof(uint32_t), c->stream);
+    p += capr * sizeof(uint16_t);
+    c->d_ord_lut = reinterpret_cast<uint16_t*>(p);
+    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, 2 * B * sizeof(uint32_t), c->stream);
     if (e != cudaSuccess) return e;
-    k_ord_table<<<(kOrdB + 1 + 255) / 256, 256, 0, c->stream>>>(c->d_rec, c->rec_words, c->val_words, c->N,
-                                                                (uint32_t)(c->hi[0] - c->lo[0]), c->d_ord_T);
-    c->launches++;
+    k_ord_table<<<((1 << c->ord_bits) + 1 + 255) / 256, 256, 0, c->stream>>>(
+        c->d_rec, c->rec_words, c->val_words, c->N, (uint32_t)(c->hi[0] - c->lo[0]), c->ord_bits, c->d_ord_T);
+    const int64_t ncell = lut_cells(c->N, &c->ord_lut_shift);
+    k_ord_lut<<<(int)std::min<int64_t>((ncell + 255) / 256, 4096), 256, 0, c->stream>>>(
+        c->d_ord_T, c->ord_bits, c->ord_lut_shift, ncell, std::max<int64_t>(c->N, 1), c->d_ord_lut);
+    c->launches += 2;
     return cudaGetLastError();
 }
 
-cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out) {
+static OrdHistArgs make_hist_args(gcp_ctx* c, const SampleArgs& sa) {
+    OrdHistArgs oh;
+    oh.sa = sa;
+    oh.lut = c->d_ord_lut;
+    oh.lut_shift = c->ord_lut_shift;
+    oh.keys = c->d_ord_key;
+    oh.ranks = c->d_ord_rank;
+    oh.totals = c->d_ord_cnt;
+    oh.bits = c->ord_bits;
+    oh.ratio = 1;
+    oh.n = sa.p + sa.q;
+    return oh;
+}
+
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, bool hist_done) {
+    const int64_t n = s.p + s.q;
+    *order_out = c->d_ord;
+    if (n == 0) return cudaSuccess;
+    const int B = 1 << c->ord_bits;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_ord_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOrdSmem);
+        cudaError_t e = cudaFuncSetAttribute(k_ord_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(((1 << kOrdMaxBits) + (1 << kOrdMaxBits) / 32) * 4));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int64_t n = s.p + s.q;
-    if (n == 0) {
-        *order_out = c->d_ord;
-        return cudaSuccess;
-    }
-    const int nc = c->sm_count;
-    const int64_t per = (n + nc - 1) / nc;
     uint32_t* totals = c->d_ord_cnt;
-    uint32_t* cursor = c->d_ord_cnt + kOrdB;
-    k_ord_hist<<<nc, kOrdThreads, kOrdSmem, c->stream>>>(s, c->d_ord_T, per, c->d_ord_key, totals);
-    k_ord_scan<<<1, kOrdThreads, 0, c->stream>>>(totals, cursor);
-    k_ord_scatter<<<nc, kOrdThreads, 0, c->stream>>>(c->d_ord_key, n, per, cursor, c->d_ord);
-    c->launches += 3;
-    *order_out = c->d_ord;
+    uint32_t* cursor = c->d_ord_cnt + (1 << kOrdMaxBits);
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+    if (!hist_done) {
+        // totals may hold an unconsumed histogram (an Adam launch prepared an
+        // iteration that did not follow): start from zero
+        cudaError_t e = cudaMemsetAsync(totals, 0, (size_t)B * sizeof(uint32_t), c->stream);
+        if (e != cudaSuccess) return e;
+        k_ord_hist<<<nb, 256, 0, c->stream>>>(make_hist_args(c, s));
+        c->launches++;
+    }
+    k_ord_scan<<<1, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(totals, cursor, B);
+    k_ord_scatter<<<nb, 256, 0, c->stream>>>(c->d_ord_key, c->d_ord_rank, n, cursor, c->d_ord);
+    c->launches += 2;
     return cudaGetLastError();
+}
+
+// The histogram pass of the next iteration for the Adam launch to carry
+// (GCP_ORD_FUSE=0 keeps it a launch of its own).
+bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh, int64_t adam_vecs) {
+    const char* fe = getenv("GCP_ORD_FUSE");
+    const bool fuse = !(fe && atoi(fe) == 0);
+    const int64_t n = next.p + next.q;
+    if (!fuse || n == 0 || n > c->ord_cap || !c->d_ord) return false;
+    *oh = make_hist_args(c, next);
+    oh->ratio = (int)std::max<int64_t>(1, adam_vecs / n);
+    return true;
 }
 
 // Fixed-order sum of n fp64 partials (deterministic; one CTA).

@@ -226,15 +226,43 @@ __global__ void k_export(const SampleArgs sa, int64_t first, int64_t count, cons
     if (att) att[i] = smp.attempts;
 }
 
+// Slot-order bucket of slot s (kernels.cu, launch_slot_order): nonzero slot ->
+// the bucket of the mode-1 row of record j = mulhi(W0, N), looked up in a
+// per-tensor table over the top bits of j (exact up to the records straddling a
+// lookup cell, which only moves a slot to a neighbouring bucket); zero slot ->
+// floor(c_1 B / I_1) of its attempt-0 candidate c_1 = mulhi(W0, I_1).
+__device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16_t* __restrict__ lut, int lut_shift,
+                                               int bits, int64_t s, uint32_t it, uint64_t inv) {
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    if (s < a.p) {
+        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, it, k0, k1);
+        const uint64_t j = range_map(w.w0, (uint64_t)a.N);
+        return __ldg(lut + (j >> lut_shift));
+    }
+    const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, it, k0, k1);
+    const uint64_t c1 = range_map(w.w0, a.bdim[0]);
+    uint64_t q = __umul64hi(c1 << bits, inv);   // floor or floor - 1 (c_1 B < 2^47)
+    if ((q + 1) * a.bdim[0] <= (c1 << bits)) ++q;
+    return (uint32_t)q;
+}
+
+// bucket of slot s and its rank inside the bucket (arrival order of a global
+// atomicAdd: the scatter then needs no reservation pass)
+__device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, uint32_t it, uint64_t inv) {
+    const uint32_t b = ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
+    oh.keys[s] = (uint16_t)b;
+    oh.ranks[s] = atomicAdd(oh.totals + b, 1u);
+}
+
 // Alg. 1 over the segments of the contiguous arrays:
 // B <- b1 B + (1-b1) g; C <- b2 C + (1-b2) g^2; A <- A - rate (B bc1)/sqrt(C bc2 + eps);
 // A <- (A < l) ? l : A; G <- 0 (fused reset).  bc = 1/(1-beta^t) from the host in fp64.
 template <typename T>
-__global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
                                               T* __restrict__ G, T* __restrict__ B, T* __restrict__ C,
                                               T rate, T b1, T b2, T eps, T bc1, T bc2, T lower,
                                               int zero_g, int R_pad, int row_stride, const DevStep* step,
-                                              long long t_off) {
+                                              long long t_off, const OrdHistArgs oh) {
     using V = typename Vec16<T>::type;
     constexpr int VE = Vec16<T>::n;
     if (step) {   // graph replay: t = t0 + offset, bias corrections in fp64 from it
@@ -243,8 +271,19 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
         bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
         bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec_total;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    // the next iteration's slot histogram (ALU work: Philox + table search)
+    // interleaved with this memory-bound stream, one slot per oh.ratio vectors
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    int64_t hs = tid;
+    const uint32_t hit = oh.n ? iter_word(oh.sa) : 0u;
+    const uint64_t hinv = oh.n && oh.sa.bdim[0] > 1 ? (~0ull) / oh.sa.bdim[0] : 0ull;
+    int hstep = 0;
+    for (int64_t i = tid; i < nvec_total; i += nt) {
+        if (hs < oh.n && ++hstep == oh.ratio) {
+            hstep = 0;
+            ord_hist_slot(oh, hs, hit, hinv);
+            hs += nt;
+        }
         // map the virtual vector index onto its segment
         int64_t rem = i;
         int sidx = 0;
@@ -278,6 +317,7 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
             *reinterpret_cast<V*>(G + ea) = z;
         }
     }
+    for (; hs < oh.n; hs += nt) ord_hist_slot(oh, hs, hit, hinv);
 }
 
 struct InitArgs {

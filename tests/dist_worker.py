@@ -25,6 +25,11 @@ def main():
     prec = "fp32" if mode == "sync32" else "fp64"
     if mode == "sync32":
         os.environ["GCP_MULTIMEM"] = "1"   # exercise the NVLS path whatever P is
+    if mode in ("sync32", "async"):
+        # the slot-ordered K2 (on by default only when mode-1 rows spill L2, e.g.
+        # c5 blocks): standalone histogram under the fused exchange (sync32), the
+        # histogram carried by the Adam launch (async)
+        os.environ["GCP_SLOT_ORDER"] = "1"
     mode = "sync" if mode == "sync32" else mode
     # TG, TE: the C18 bounds (gradient per element vs the rounding scale S, loss
     # estimate vs sum |terms|) from an identical state.  TM / TM_FIT / TE_FIT bound

@@ -20,6 +20,10 @@ def test_reference_arm_json_line():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in j, key
     assert j["impl"] == "reference" and j["unit"] == "epochs/s" and j["value"] > 0
-    assert j["cpu_baseline"]["kind"] == "oracle" and j["cpu_baseline"]["cores"] == 1
+    import os
+    assert j["cpu_baseline"]["kind"] == "oracle" and j["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+    assert j["cpu_baseline"]["cpu_model"] and "OMP_NUM_THREADS" in j["cpu_baseline"]
+    # the line reports what it timed: K steps of ms_per_step fit in the run's wall time
+    assert j["steps"] * j["ms_per_step"] <= j["wall_s"] * 1e3
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["value"] == j["value"]
     assert j["config"]["workload"].startswith("c1")

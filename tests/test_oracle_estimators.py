@@ -260,3 +260,25 @@ def test_async_replicas_identical_after_sync(orc):
             lo, hi = blocks[grp[0]].lo[k], blocks[grp[0]].hi[k]
             for w in grp[1:]:
                 assert np.array_equal(Aw[w][k][lo:hi], Aw[grp[0]][k][lo:hi])
+
+
+@pytest.mark.parametrize("nthreads", [1, 3, 8])
+def test_openmp_timing_variant_matches_serial(orc, nthreads):
+    """The OpenMP variant timed as the CPU baseline
+    computes the serial oracle's estimator: same draws, sums reordered only."""
+    dims, subs, v, A = _fixture("poisson", dims=(9, 8, 7), nnz=60, seed=31)
+    t = orc.Tensor(dims, subs, v)
+    G, _, ls = orc.sampled_grad(t, A, "poisson", 5, 0, 3, 301, 457, with_scale=False)
+    Gp, lp = orc.sampled_grad_par(t, A, "poisson", 5, 0, 3, 301, 457, nthreads=nthreads)
+    for a, b in zip(G, Gp):
+        assert np.allclose(a, b, rtol=1e-12, atol=1e-12 * np.abs(a).max())
+    assert lp == pytest.approx(ls, rel=1e-12)
+    e, _ = orc.loss_estimate(t, A, "poisson", 9, 0, 200, 300)
+    assert orc.loss_estimate_par(t, A, "poisson", 9, 0, 200, 300, nthreads=nthreads) == pytest.approx(e, rel=1e-12)
+    flat = np.concatenate([a.ravel() for a in A])
+    g = np.concatenate([a.ravel() for a in G])
+    a1, b1, c1 = flat.copy(), np.zeros_like(flat), np.zeros_like(flat)
+    a2, b2, c2 = flat.copy(), np.zeros_like(flat), np.zeros_like(flat)
+    orc.adam(a1, g, b1, c1, 1, 1e-2, lower=0.0)
+    orc.adam_par(a2, g, b2, c2, 1, 1e-2, lower=0.0, nthreads=nthreads)
+    assert np.array_equal(a1, a2) and np.array_equal(b1, b2) and np.array_equal(c1, c2)
