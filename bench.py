@@ -309,6 +309,8 @@ def main():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--mode", default="sync", choices=["sync", "twosided", "async", "fedadam"])
     ap.add_argument("--tau", type=int, default=10)
+    ap.add_argument("--samples", type=float, default=None,
+                    help="override p = q per iteration (global), e.g. the all-reduce vs two-sided crossover sweep")
     ap.add_argument("--cpu-sample", type=int, default=100_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -325,6 +327,8 @@ def main():
 
     name = args.config
     w = workload(name)
+    if args.samples:
+        w["s"] = int(args.samples)
     dev = local
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
@@ -544,6 +548,7 @@ def hbm_gate(g, dev, stream, args, peak, peak_src, epochs=3, warmup=3):
     w = workload("c4")
     t0 = time.time()
     subs, vals, gen_s = make_tensor("c4", f"cuda:{dev}")
+    torch.cuda.empty_cache()   # the generator's temporaries: the ingest scratch needs the room
     ctx = g.Context(dev, stream.cuda_stream, args.precision)
     ctx.tensor_create_ptr(w["dims"], len(vals), subs.data_ptr(), vals.data_ptr())
     del subs, vals

@@ -207,7 +207,7 @@ ModelArgs model_args(const gcp_ctx* c) {
 // the slot-order buffers (their table T is per tensor: dropped with the tensor)
 void ord_free(gcp_ctx* c) {
     graph_drop(c);
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     gfree(c, c->d_ord_buf);
     c->d_ord_buf = nullptr;
     c->d_ord_T = nullptr;
@@ -295,6 +295,7 @@ gcp_status checkpoint_restore(gcp_ctx* c) {
     CUDA_TRY(c, cudaMemcpyAsync(c->d_C, c->d_Cck, bytes, cudaMemcpyDeviceToDevice, c->stream), "restore");
     if (!c->ag_interleaved) CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "restore");
     if (c->fused) CUDA_TRY(c, cudaMemsetAsync(c->d_G2, 0, bytes, c->stream), "restore");
+    if (c->d_bm) CUDA_TRY(c, cudaMemsetAsync(c->d_bm, 0, tsn_bitmap_bytes(c), c->stream), "restore");
     c->t = c->t_ck;
     c->ts = c->ts_ck;
     return GCP_OK;
@@ -655,8 +656,11 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         c->slot_order = oenv ? atoi(oenv) != 0 : m1_spills;
     }
     const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
-    const bool use_fused = fused_possible(c);
-    if (use_fused) ST_TRY(fused_alloc(c, bytes));   // A, G, G2: symmetric NVLink windows
+    // sync: the fused NVLink exchange; two-sided: the device-driven import /
+    // export (twosided_nvl.cu); both keep A, G, G2 in symmetric NVLink windows
+    const bool use_fused = fused_possible(c) || tsn_possible(c);
+    if (use_fused) ST_TRY(fused_alloc(c, bytes));
+    if (use_fused && two_sided(c)) ST_TRY(tsn_alloc_bitmap(c));
     {
         void** bufs[] = {&c->d_A, &c->d_B, &c->d_C};
         for (void** b : bufs) {
@@ -709,7 +713,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     c->t = 0;
     c->ts = 0;
     c->it = 0;
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     c->grad_blocks = sample_kernel_blocks(c);
     ST_TRY(ensure_partials(c, c->grad_blocks));
     c->have_model = true;
@@ -796,7 +800,7 @@ gcp_status gcp_sample(gcp_ctx* c, gcp_strategy strategy, int64_t s_nz, int64_t s
     c->q_w = q_w;
     c->seed = seed;
     c->bound = true;
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     graph_drop(c);
     return GCP_OK;
 }
@@ -854,7 +858,7 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     const int stratified = c->strategy == GCP_STRATIFIED;
     const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
     // two-sided layout (row f3): touch pass + import of the rows owned elsewhere
-    if (two_sided(c) && !c->have_grad) ST_TRY(twosided_import(c, s));
+    if (two_sided(c) && !c->have_grad) ST_TRY(c->fused ? tsn_import(c, s) : twosided_import(c, s));
     const ModelArgs m = model_args(c);
     const int with_loss = sampled_loss_out != nullptr;
     cudaEvent_t ev;
@@ -879,19 +883,34 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
             }
         }
         if (c->slot_order && n_slots <= c->ord_cap) {
-            // the histogram pass may have run inside the previous Adam launch
-            const bool done = c->ord_hist_ready && c->ord_hist_it == c->it;
-            prof_begin(c, PROF_OTHER, &ev);
-            CUDA_TRY(c, launch_slot_order(c, s, &so.order, done), "slot order");
-            prof_end(c, PROF_OTHER, ev);
+            // the previous iteration's K2 / Adam may have prepared this order
+            const int stage = c->ord_stage_it == c->it ? c->ord_stage : 0;
+            if (stage < 2) {
+                prof_begin(c, PROF_OTHER, &ev);
+                CUDA_TRY(c, launch_slot_order(c, s, &so.order, stage), "slot order");
+                prof_end(c, PROF_OTHER, ev);
+            } else {
+                so.order = c->d_ord;
+            }
         }
-        c->ord_hist_ready = false;
+    }
+    c->ord_stage = 0;
+    // the gradient K2 carries the next iteration's slot histogram
+    OrdHistArgs oh;
+    bool carry = false;
+    if (so.order) {
+        const SampleArgs nx = sample_args(c, c->p_w, c->q_w, c->seed, c->it + 1, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
+        carry = ord_hist_args(c, nx, &oh);
     }
     prof_begin(c, PROF_GRAD, &ev);
     CUDA_TRY(c, launch_sample_kernel(c, so, m, loss, 0, !stratified, weight_nz(c, c->p_w), weight_z(c, c->q_w),
-                                     with_loss, c->d_partials, c->grad_blocks),
+                                     with_loss, c->d_partials, c->grad_blocks, carry ? &oh : nullptr),
              "gcp_loss_grad");
     prof_end(c, PROF_GRAD, ev);
+    if (carry) {
+        c->ord_stage = 1;
+        c->ord_stage_it = c->it + 1;
+    }
     c->have_grad = true;
     if (with_loss) {
         prof_begin(c, PROF_OTHER, &ev);
@@ -916,8 +935,9 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
         return set_error(GCP_E_ARG, "gcp_adam_step: need 0 <= beta < 1, eps > 0, rate >= 0");
     const double lower = std::isnan(p->lower) ? loss_lower(c->last_loss) : p->lower;
     c->t += 1;
-    if (c->fused) {   // sync P > 1: reduce-scatter + Adam + all-gather in one NVLink kernel
-        ST_TRY(fused_exchange(c, p, lower));
+    if (c->fused) {   // sync P > 1: reduce-scatter + Adam + all-gather in one NVLink kernel;
+                      // two-sided: export of the touched rows + Adam on the owned rows
+        ST_TRY(two_sided(c) ? tsn_export(c, p, lower) : fused_exchange(c, p, lower));
         c->it += 1;
         c->have_grad = false;
         return GCP_OK;
@@ -952,26 +972,25 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
         seg.len[0] = c->n_coef;
         seg.n = 1;
     }
-    // the next iteration's slot-order histogram rides along in this (memory-bound) launch
-    OrdHistArgs oh;
-    oh.n = 0;
-    bool fused_hist = false;
-    if (c->slot_order && !two_sided(c) && c->bound && c->ord_cap > 0) {
+    // the next iteration's slot-order scan (launched here) and scatter (carried
+    // by this memory-bound Adam launch), when its histogram is ready
+    OrdScatterArgs os;
+    bool carry = false;
+    cudaEvent_t ev;
+    if (c->ord_stage == 1 && c->ord_stage_it == c->it + 1) {
         int64_t vecs = 0;
         for (int i = 0; i < seg.n; ++i) vecs += seg.len[i] / (c->prec == GCP_FP32 ? 4 : 2);
-        const SampleArgs nx = sample_args(c, c->p_w, c->q_w, c->seed, c->it + 1, KIND_GRAD_NZ, KIND_GRAD_Z,
-                                          c->strategy == GCP_STRATIFIED);
-        fused_hist = ord_hist_args(c, nx, &oh, vecs);
+        prof_begin(c, PROF_OTHER, &ev);
+        carry = ord_scatter_args(c, c->p_w + c->q_w, &os, vecs);
+        prof_end(c, PROF_OTHER, ev);
     }
-    cudaEvent_t ev;
     prof_begin(c, PROF_ADAM, &ev);
     CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower,
                             c->capturing ? c->t - c->graph_t0 : c->t, sharded ? 0 : 1, c->ag_stride,
-                            c->capturing ? c->d_step : nullptr, fused_hist ? &oh : nullptr),
+                            c->capturing ? c->d_step : nullptr, carry ? &os : nullptr),
              "gcp_adam_step");
     prof_end(c, PROF_ADAM, ev);
-    c->ord_hist_ready = fused_hist;
-    c->ord_hist_it = c->it + 1;
+    if (carry) c->ord_stage = 2;
     if (sharded) {
         CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, (size_t)c->n_coef * tsz(c), c->stream), "adam G reset");
         if (!two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // two-sided: rows stay partitioned
@@ -1037,11 +1056,12 @@ gcp_status gcp_fit_begin(gcp_ctx* c, const gcp_fit_params* p, double* initial_es
 // uploaded to device memory; each captured launch adds its own offset, so the
 // replay needs no host work per iteration.  Not used on
 // the legacy stream (uncapturable), while profiling (per-kernel events), for
-// the two-sided layout (host-sized transfers) or FedAdam (host server clock).
+// the NCCL two-sided layout (host-sized transfers; the device-driven one over
+// NVLink windows replays) or FedAdam (host server clock).
 static bool graph_ok(const gcp_ctx* c) {
     const char* env = getenv("GCP_GRAPHS");
     if (env && atoi(env) == 0) return false;
-    return c->stream != nullptr && !c->prof_on && !two_sided(c) && c->mode != GCP_DIST_ASYNC_FEDADAM;
+    return c->stream != nullptr && !c->prof_on && (!two_sided(c) || c->fused) && c->mode != GCP_DIST_ASYNC_FEDADAM;
 }
 
 static gcp_status epoch_graph(gcp_ctx* c, gcp_loss loss, const gcp_adam_params& ap, int iters) {

@@ -56,8 +56,10 @@ struct SampleOcc {
 template <typename T>
 cudaError_t sample_kernel_T(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss, int loss_mode,
                             int semi_nz, double w_nz, double w_z, int with_loss, double* partials,
-                            int nblocks) {
+                            int nblocks, const OrdHistArgs* oh) {
     KParams<T> kp;
+    if (oh) kp.oh = *oh;
+    else memset(&kp.oh, 0, sizeof(kp.oh));
     kp.loss = loss; kp.loss_mode = loss_mode; kp.semi_nz = semi_nz; kp.with_loss = with_loss;
     kp.w_nz = (T)w_nz; kp.w_z = (T)w_z; kp.partials = partials;
     const int nvec = m.R_pad / Vec16<T>::n;
@@ -87,20 +89,20 @@ cudaError_t export_T(gcp_ctx* c, const SampleArgs& s, int64_t first, int64_t cou
 template <typename T>
 cudaError_t adam_T(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                    double beta1, double beta2, double eps, double lower, int64_t t, int zero_g, int R_pad,
-                   int row_stride, const DevStep* step, const OrdHistArgs* oh) {
+                   int row_stride, const DevStep* step, const OrdScatterArgs* os) {
     const double bc1 = 1.0 / (1.0 - pow(beta1, (double)t));
     const double bc2 = 1.0 / (1.0 - pow(beta2, (double)t));
     int64_t nvec = 0;
     for (int i = 0; i < seg.n; ++i) nvec += seg.len[i] / Vec16<T>::n;
-    OrdHistArgs noh;
-    noh.n = 0;
-    if (nvec == 0 && !(oh && oh->n)) return cudaSuccess;
+    OrdScatterArgs nos;
+    memset(&nos, 0, sizeof(nos));
+    if (nvec == 0 && !(os && os->n)) return cudaSuccess;
     int64_t nb = (std::max<int64_t>(nvec, 1) + 255) / 256;
     const int64_t cap = (int64_t)c->sm_count * 8;
     if (nb > cap) nb = cap;
     k_adam<T><<<(int)nb, 256, 0, c->stream>>>(seg, nvec, (T*)A, (T*)G, (T*)B, (T*)C, (T)rate, (T)beta1,
                                               (T)beta2, (T)eps, (T)bc1, (T)bc2, (T)lower, zero_g, R_pad, row_stride, step,
-                                              (long long)t, oh ? *oh : noh);
+                                              (long long)t, os ? *os : nos);
     return cudaGetLastError();
 }
 

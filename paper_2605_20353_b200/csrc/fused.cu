@@ -315,10 +315,29 @@ gcp_status fused_alloc(gcp_ctx* c, size_t bytes) {
     return GCP_OK;
 }
 
+// Two-sided over NVLink (twosided_nvl.cu): the touched-row bits of both
+// parities in a symmetric window of their own, zeroed.
+gcp_status tsn_alloc_bitmap(gcp_ctx* c) {
+    const size_t wb = round_win(std::max<size_t>(tsn_bitmap_bytes(c), 64));
+    NCCL_TRY_F(c, ncclMemAlloc(&c->d_bm, wb), "ncclMemAlloc");
+    NCCL_TRY_F(c, ncclCommWindowRegister(c->world, c->d_bm, wb, &c->winBM, NCCL_WIN_COLL_SYMMETRIC),
+               "ncclCommWindowRegister");
+    if (cudaMemsetAsync(c->d_bm, 0, wb, c->stream) != cudaSuccess)
+        return set_error(GCP_E_CUDA, "two-sided bits: memset failed");
+    return GCP_OK;
+}
+
 static void fused_trace_print(gcp_ctx* c);
 
 void fused_free(gcp_ctx* c) {
     if (!c->fused) return;
+    if (c->winBM) {
+        cudaStreamSynchronize(c->stream);
+        ncclCommWindowDeregister(c->world, c->winBM);
+        ncclMemFree(c->d_bm);
+        c->winBM = nullptr;
+        c->d_bm = nullptr;
+    }
     fused_trace_print(c);
     if (c->ftrace) gfree(c, c->ftrace);
     c->ftrace = nullptr;

@@ -76,8 +76,8 @@ struct ModelArgs {
     int row_stride;           // elements between consecutive rows (R_pad, or 2 R_pad when A/G interleave)
 };
 
-// The slot-order histogram pass of the NEXT iteration, fused into the Adam
-// kernel of this one (kernels.cu, launch_slot_order): n = 0 means none.
+// The slot-order histogram pass of the NEXT iteration, carried by the gradient
+// K2 of this one (kernels.cu, launch_slot_order): n = 0 means none.
 struct OrdHistArgs {
     SampleArgs sa;            // the next iteration's sampler arguments
     const uint16_t* lut;      // per-tensor lookup: bucket of nonzero index j = lut[j >> lut_shift]
@@ -86,8 +86,18 @@ struct OrdHistArgs {
     uint32_t* ranks;          // rank of the slot inside its bucket (out)
     uint32_t* totals;         // bucket totals (global atomicAdd)
     int bits;                 // log2 bucket count
-    int ratio;                // one slot per `ratio` Adam vectors of a thread
     int64_t n;                // slots (p + q)
+};
+
+// The scatter pass of the next iteration's slot order, carried by the Adam
+// launch of this one: order[cursor[key] + rank] = slot.  n = 0 means none.
+struct OrdScatterArgs {
+    const uint16_t* keys;
+    const uint32_t* ranks;
+    const uint32_t* cursor;
+    uint32_t* order;
+    int64_t n;
+    int ratio;                // one slot per `ratio` Adam vectors of a thread
 };
 
 struct Segment {              // contiguous ranges of the coefficient arrays (Adam)
@@ -129,6 +139,8 @@ struct gcp_ctx {
     ncclDevComm devcomm{};
     ncclWindow_t winA = nullptr, winG[2] = {nullptr, nullptr};
     void* d_G2 = nullptr;                         // second G buffer (iteration parity)
+    void* d_bm = nullptr;                         // two-sided over NVLink: touched-row bits (2 parities)
+    ncclWindow_t winBM = nullptr;
     // windows of the previous model kept registered for the next one of the same
     // size (a replace-ingest job skips the collective deregister / register)
     void* fcache_buf[3] = {nullptr, nullptr, nullptr};
@@ -202,8 +214,8 @@ struct gcp_ctx {
     uint32_t* d_ord_rank = nullptr;     // rank of the slot inside its bucket
     int64_t ord_cap = 0;
     int ord_bits = 15;                  // log2 of the bucket count (GCP_ORD_BITS)
-    bool ord_hist_ready = false;        // the histogram pass of iteration ord_hist_it ran inside an Adam launch
-    uint32_t ord_hist_it = 0;
+    int ord_stage = 0;                  // slot order of iteration ord_stage_it prepared by earlier launches:
+    uint32_t ord_stage_it = 0;          // 1 histogram (in K2), 2 scan + scatter too (in Adam), 0 nothing
     int slot_order = 0;                 // decided in gcp_model_init (GCP_SLOT_ORDER overrides)
     cudaGraphExec_t graph_exec = nullptr;
     double graph_key[8] = {0};
@@ -250,11 +262,13 @@ void prof_end(gcp_ctx* c, int which, cudaEvent_t ev);
 // kernels.cu launchers (enqueue on c->stream; return cudaGetLastError())
 cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss,
                                  int loss_mode, int semi_nz, double w_nz, double w_z, int with_loss,
-                                 double* partials, int nblocks);
+                                 double* partials, int nblocks,
+                                 const OrdHistArgs* oh = nullptr);   // next iteration's slot histogram
 size_t slot_order_bytes(int64_t cap);
 cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap);   // carve buffers, build the per-tensor table
-cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, bool hist_done);
-bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh, int64_t adam_vecs);
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, int stage);
+bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh);
+bool ord_scatter_args(gcp_ctx* c, int64_t n, OrdScatterArgs* os, int64_t adam_vecs);   // + launches the scan
 cudaError_t launch_reduce_partials(gcp_ctx* c, const double* partials, int n, double* out);
 cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);
@@ -262,7 +276,7 @@ cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* 
                         double rate, double beta1, double beta2, double eps, double lower,
                         int64_t t, int zero_g, int row_stride = 0,    // row_stride 0: contiguous A/G
                         const DevStep* step = nullptr,                // step: t = step->t + t (offset), rate
-                        const OrdHistArgs* oh = nullptr);             // fused next-iteration slot histogram
+                        const OrdScatterArgs* os = nullptr);          // fused next-iteration slot scatter
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
 cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);
@@ -294,6 +308,13 @@ gcp_status fused_alloc(gcp_ctx* c, size_t bytes);   // A, G, G2 as symmetric win
 void fused_free(gcp_ctx* c);
 void fused_cache_release(gcp_ctx* c);   // collective: deregister the kept windows
 gcp_status fused_exchange(gcp_ctx* c, const gcp_adam_params* p, double lower);
+gcp_status tsn_alloc_bitmap(gcp_ctx* c);          // two-sided over NVLink: the bit window (collective)
+
+// twosided_nvl.cu (row f3 driven by the device over the symmetric windows)
+bool tsn_possible(gcp_ctx* c);
+size_t tsn_bitmap_bytes(const gcp_ctx* c);
+gcp_status tsn_import(gcp_ctx* c, const SampleArgs& sa);
+gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower);
 
 }  // namespace gcp
 

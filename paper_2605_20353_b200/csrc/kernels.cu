@@ -8,9 +8,9 @@
 namespace gcp {
 
 cudaError_t sample_kernel_f32(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
-                              int, double*, int);
+                              int, double*, int, const OrdHistArgs*);
 cudaError_t sample_kernel_f64(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
-                              int, double*, int);
+                              int, double*, int, const OrdHistArgs*);
 int sample_occupancy_f32(int, int);
 int sample_occupancy_f64(int, int);
 cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
@@ -18,9 +18,9 @@ cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int6
 cudaError_t export_f64(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
                        int32_t*);
 cudaError_t adam_f32(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int, const DevStep*, const OrdHistArgs*);
+                     double, int64_t, int, int, int, const DevStep*, const OrdScatterArgs*);
 cudaError_t adam_f64(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int, const DevStep*, const OrdHistArgs*);
+                     double, int64_t, int, int, int, const DevStep*, const OrdScatterArgs*);
 cudaError_t init_f32(gcp_ctx*, const InitArgs&, void*);
 cudaError_t init_f64(gcp_ctx*, const InitArgs&, void*);
 
@@ -31,10 +31,10 @@ int sample_kernel_blocks(gcp_ctx* c) {
 
 cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss, int loss_mode,
                                  int semi_nz, double w_nz, double w_z, int with_loss, double* partials,
-                                 int nblocks) {
+                                 int nblocks, const OrdHistArgs* oh) {
     return c->prec == GCP_FP32
-               ? sample_kernel_f32(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks)
-               : sample_kernel_f64(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks);
+               ? sample_kernel_f32(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh)
+               : sample_kernel_f64(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh);
 }
 
 cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
@@ -46,11 +46,11 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
 
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                         double beta1, double beta2, double eps, double lower, int64_t t, int zero_g,
-                        int row_stride, const DevStep* step, const OrdHistArgs* oh) {
+                        int row_stride, const DevStep* step, const OrdScatterArgs* os) {
     const int rs = row_stride > 0 ? row_stride : c->R_pad;
     return c->prec == GCP_FP32
-               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, oh)
-               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, oh);
+               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, os)
+               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, os);
 }
 
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
@@ -78,12 +78,14 @@ cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
 // accesses walk the records and rows forward.
 //   histogram      per slot: Philox word -> bucket (kernels.cuh ord_bucket) and
 //                  the slot's rank inside its bucket (a global atomicAdd);
-//                  carried by the previous iteration's Adam launch (k_adam,
-//                  OrdHistArgs: ALU work inside a memory-bound stream), else
-//                  k_ord_hist
+//                  carried by the previous iteration's gradient K2 (OrdHistArgs:
+//                  ALU work under its memory-bound gathers), else k_ord_hist
 //   k_ord_scan     one CTA: exclusive scan of the bucket totals -> cursors;
 //                  totals reset for the next iteration
-//   k_ord_scatter  order[cursor[bucket] + rank] = slot
+//   k_ord_scatter  order[cursor[bucket] + rank] = slot (GCP_ORD_FUSE=2 carries
+//                  it in the previous Adam launch instead: slower, see
+//                  ord_scatter_args)
+// So in steady state an iteration launches the scan and the scatter.
 // Order inside a bucket is the atomics' arrival order (run to run it varies),
 // which only moves the fp32 atomic summation order of K2.
 constexpr int kOrdMaxBits = 15;            // table / counter capacity
@@ -129,8 +131,8 @@ __global__ void k_ord_lut(const int64_t* __restrict__ T, int bits, int shift, in
     }
 }
 
-// Histogram pass for an iteration whose histogram no Adam launch computed (the
-// first of an epoch graph, eager calls; otherwise k_adam carries it):
+// Histogram pass for an iteration whose histogram no gradient K2 computed (the
+// first of an epoch graph, eager calls):
 // bucket and in-bucket rank of every slot, four slots per thread in flight.
 __global__ void __launch_bounds__(256) k_ord_hist(const OrdHistArgs oh) {
     const uint32_t it = iter_word(oh.sa);
@@ -253,16 +255,11 @@ static OrdHistArgs make_hist_args(gcp_ctx* c, const SampleArgs& sa) {
     oh.ranks = c->d_ord_rank;
     oh.totals = c->d_ord_cnt;
     oh.bits = c->ord_bits;
-    oh.ratio = 1;
     oh.n = sa.p + sa.q;
     return oh;
 }
 
-cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, bool hist_done) {
-    const int64_t n = s.p + s.q;
-    *order_out = c->d_ord;
-    if (n == 0) return cudaSuccess;
-    const int B = 1 << c->ord_bits;
+static cudaError_t ord_scan(gcp_ctx* c) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_ord_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -270,32 +267,65 @@ cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** 
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    const int B = 1 << c->ord_bits;
+    k_ord_scan<<<1, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(c->d_ord_cnt, c->d_ord_cnt + (1 << kOrdMaxBits),
+                                                                        B);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+// The order of this iteration's slots, from whatever the previous launches
+// prepared: stage 2 = nothing left, 1 = scan + scatter, 0 = everything.
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, int stage) {
+    const int64_t n = s.p + s.q;
+    *order_out = c->d_ord;
+    if (n == 0 || stage >= 2) return cudaSuccess;
+    const int B = 1 << c->ord_bits;
     uint32_t* totals = c->d_ord_cnt;
-    uint32_t* cursor = c->d_ord_cnt + (1 << kOrdMaxBits);
     const int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
-    if (!hist_done) {
-        // totals may hold an unconsumed histogram (an Adam launch prepared an
-        // iteration that did not follow): start from zero
+    if (stage < 1) {
+        // totals may hold an unconsumed histogram (a K2 prepared an iteration
+        // that did not follow): start from zero
         cudaError_t e = cudaMemsetAsync(totals, 0, (size_t)B * sizeof(uint32_t), c->stream);
         if (e != cudaSuccess) return e;
         k_ord_hist<<<nb, 256, 0, c->stream>>>(make_hist_args(c, s));
         c->launches++;
     }
-    k_ord_scan<<<1, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(totals, cursor, B);
-    k_ord_scatter<<<nb, 256, 0, c->stream>>>(c->d_ord_key, c->d_ord_rank, n, cursor, c->d_ord);
-    c->launches += 2;
+    cudaError_t e = ord_scan(c);
+    if (e != cudaSuccess) return e;
+    k_ord_scatter<<<nb, 256, 0, c->stream>>>(c->d_ord_key, c->d_ord_rank, n, c->d_ord_cnt + (1 << kOrdMaxBits),
+                                             c->d_ord);
+    c->launches++;
     return cudaGetLastError();
 }
 
-// The histogram pass of the next iteration for the Adam launch to carry
-// (GCP_ORD_FUSE=0 keeps it a launch of its own).
-bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh, int64_t adam_vecs) {
+// The histogram of the next iteration for the gradient K2 to carry
+// (GCP_ORD_FUSE=0 keeps every pass a launch of its own; the histogram's Philox
+// and table lookups cost K2 nothing measurable on c4).
+bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh) {
     const char* fe = getenv("GCP_ORD_FUSE");
-    const bool fuse = !(fe && atoi(fe) == 0);
+    if ((fe && atoi(fe) == 0) || !c->d_ord) return false;
     const int64_t n = next.p + next.q;
-    if (!fuse || n == 0 || n > c->ord_cap || !c->d_ord) return false;
+    if (n == 0 || n > c->ord_cap) return false;
     *oh = make_hist_args(c, next);
-    oh->ratio = (int)std::max<int64_t>(1, adam_vecs / n);
+    return true;
+}
+
+// The scan of the next iteration (launched here) and its scatter for the Adam
+// launch to carry -- only with GCP_ORD_FUSE=2: the random 4-B stores slowed
+// Adam's stream by more than the scatter launch costs (c4: Adam 0.70 -> 1.07 ms
+// against a 0.2-ms scatter, profiles/r02_summary.md).
+bool ord_scatter_args(gcp_ctx* c, int64_t n, OrdScatterArgs* os, int64_t adam_vecs) {
+    const char* fe = getenv("GCP_ORD_FUSE");
+    if (!(fe && atoi(fe) == 2)) return false;
+    if (!c->d_ord || n == 0 || n > c->ord_cap) return false;
+    if (ord_scan(c) != cudaSuccess) return false;
+    os->keys = c->d_ord_key;
+    os->ranks = c->d_ord_rank;
+    os->cursor = c->d_ord_cnt + (1 << kOrdMaxBits);
+    os->order = c->d_ord;
+    os->n = n;
+    os->ratio = (int)std::max<int64_t>(1, adam_vecs / n);
     return true;
 }
 

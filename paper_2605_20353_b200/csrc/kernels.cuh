@@ -23,6 +23,7 @@ template <> struct Vec16<float> { using type = float4; static constexpr int n = 
 template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
 
 template <typename T> struct KParams {
+    OrdHistArgs oh;   // gradient launches: the next iteration's slot histogram (oh.n = 0: none)
     int loss;
     int loss_mode;    // 1: loss estimate only (no scatter)
     int semi_nz;      // 1: semi-stratified nonzero value w (f'(x,m) - f'(0,m))
@@ -52,6 +53,34 @@ template <>
 __device__ __forceinline__ void ldg_vec<double, 2>(double (&dst)[2], const double* src) {
     const double2 v = __ldg(reinterpret_cast<const double2*>(src));
     dst[0] = v.x; dst[1] = v.y;
+}
+
+// Slot-order bucket of slot s (kernels.cu, launch_slot_order): nonzero slot ->
+// the bucket of the mode-1 row of record j = mulhi(W0, N), looked up in a
+// per-tensor table over the top bits of j (exact up to the records straddling a
+// lookup cell, which only moves a slot to a neighbouring bucket); zero slot ->
+// floor(c_1 B / I_1) of its attempt-0 candidate c_1 = mulhi(W0, I_1).
+__device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16_t* __restrict__ lut, int lut_shift,
+                                               int bits, int64_t s, uint32_t it, uint64_t inv) {
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    if (s < a.p) {
+        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, it, k0, k1);
+        const uint64_t j = range_map(w.w0, (uint64_t)a.N);
+        return __ldg(lut + (j >> lut_shift));
+    }
+    const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, it, k0, k1);
+    const uint64_t c1 = range_map(w.w0, a.bdim[0]);
+    uint64_t q = __umul64hi(c1 << bits, inv);   // floor or floor - 1 (c_1 B < 2^47)
+    if ((q + 1) * a.bdim[0] <= (c1 << bits)) ++q;
+    return (uint32_t)q;
+}
+
+// bucket of slot s and its rank inside the bucket (arrival order of a global
+// atomicAdd: the scatter then needs no reservation pass)
+__device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, uint32_t it, uint64_t inv) {
+    const uint32_t b = ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
+    oh.keys[s] = (uint16_t)b;
+    oh.ranks[s] = atomicAdd(oh.totals + b, 1u);
 }
 
 // One warp takes 32 consecutive slots: each lane draws one sample (index work
@@ -109,6 +138,8 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
     }
 
     double lacc = 0.0;
+    const uint32_t hit = kp.oh.n ? iter_word(kp.oh.sa) : 0u;
+    const uint64_t hinv = kp.oh.n && kp.oh.sa.bdim[0] > 1 ? (~0ull) / kp.oh.sa.bdim[0] : 0ull;
     // software pipeline: the next chunk's record / first-bucket loads are in
     // flight while this chunk's rows are gathered and scattered
     Pending<D> nxt = issue_sample<T, D>(sa, slot_at(sa, (warp0 << 5) + lane, total));
@@ -126,6 +157,9 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
         }
         const T wv = smp.nz ? kp.w_nz : kp.w_z;
         const int flags = (valid ? 1 : 0) | (smp.nz ? 2 : 0);
+        if (kp.oh.n) {   // next iteration's histogram: slot s (natural order), ALU work under this chunk's loads
+            if (s < kp.oh.n) ord_hist_slot(kp.oh, s, hit, hinv);
+        }
 
 #pragma unroll
         for (int r0 = 0; r0 < GL; r0 += RB) {
@@ -226,34 +260,6 @@ __global__ void k_export(const SampleArgs sa, int64_t first, int64_t count, cons
     if (att) att[i] = smp.attempts;
 }
 
-// Slot-order bucket of slot s (kernels.cu, launch_slot_order): nonzero slot ->
-// the bucket of the mode-1 row of record j = mulhi(W0, N), looked up in a
-// per-tensor table over the top bits of j (exact up to the records straddling a
-// lookup cell, which only moves a slot to a neighbouring bucket); zero slot ->
-// floor(c_1 B / I_1) of its attempt-0 candidate c_1 = mulhi(W0, I_1).
-__device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16_t* __restrict__ lut, int lut_shift,
-                                               int bits, int64_t s, uint32_t it, uint64_t inv) {
-    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-    if (s < a.p) {
-        const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, it, k0, k1);
-        const uint64_t j = range_map(w.w0, (uint64_t)a.N);
-        return __ldg(lut + (j >> lut_shift));
-    }
-    const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, it, k0, k1);
-    const uint64_t c1 = range_map(w.w0, a.bdim[0]);
-    uint64_t q = __umul64hi(c1 << bits, inv);   // floor or floor - 1 (c_1 B < 2^47)
-    if ((q + 1) * a.bdim[0] <= (c1 << bits)) ++q;
-    return (uint32_t)q;
-}
-
-// bucket of slot s and its rank inside the bucket (arrival order of a global
-// atomicAdd: the scatter then needs no reservation pass)
-__device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, uint32_t it, uint64_t inv) {
-    const uint32_t b = ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
-    oh.keys[s] = (uint16_t)b;
-    oh.ranks[s] = atomicAdd(oh.totals + b, 1u);
-}
-
 // Alg. 1 over the segments of the contiguous arrays:
 // B <- b1 B + (1-b1) g; C <- b2 C + (1-b2) g^2; A <- A - rate (B bc1)/sqrt(C bc2 + eps);
 // A <- (A < l) ? l : A; G <- 0 (fused reset).  bc = 1/(1-beta^t) from the host in fp64.
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) k_adam(const Segm
                                               T* __restrict__ G, T* __restrict__ B, T* __restrict__ C,
                                               T rate, T b1, T b2, T eps, T bc1, T bc2, T lower,
                                               int zero_g, int R_pad, int row_stride, const DevStep* step,
-                                              long long t_off, const OrdHistArgs oh) {
+                                              long long t_off, const OrdScatterArgs os) {
     using V = typename Vec16<T>::type;
     constexpr int VE = Vec16<T>::n;
     if (step) {   // graph replay: t = t0 + offset, bias corrections in fp64 from it
@@ -271,17 +277,15 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) k_adam(const Segm
         bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
         bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
     }
-    // the next iteration's slot histogram (ALU work: Philox + table search)
-    // interleaved with this memory-bound stream, one slot per oh.ratio vectors
+    // the next iteration's slot-order scatter (random 4-B stores into L2)
+    // interleaved with this memory-bound stream, one slot per os.ratio vectors
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     int64_t hs = tid;
-    const uint32_t hit = oh.n ? iter_word(oh.sa) : 0u;
-    const uint64_t hinv = oh.n && oh.sa.bdim[0] > 1 ? (~0ull) / oh.sa.bdim[0] : 0ull;
     int hstep = 0;
     for (int64_t i = tid; i < nvec_total; i += nt) {
-        if (hs < oh.n && ++hstep == oh.ratio) {
+        if (hs < os.n && ++hstep == os.ratio) {
             hstep = 0;
-            ord_hist_slot(oh, hs, hit, hinv);
+            os.order[__ldg(os.cursor + os.keys[hs]) + os.ranks[hs]] = (uint32_t)hs;
             hs += nt;
         }
         // map the virtual vector index onto its segment
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) k_adam(const Segm
             *reinterpret_cast<V*>(G + ea) = z;
         }
     }
-    for (; hs < oh.n; hs += nt) ord_hist_slot(oh, hs, hit, hinv);
+    for (; hs < os.n; hs += nt) os.order[__ldg(os.cursor + os.keys[hs]) + os.ranks[hs]] = (uint32_t)hs;
 }
 
 struct InitArgs {

@@ -30,6 +30,9 @@ def main():
         # c5 blocks): standalone histogram under the fused exchange (sync32), the
         # histogram carried by the Adam launch (async)
         os.environ["GCP_SLOT_ORDER"] = "1"
+    if mode == "twosided_nccl":
+        os.environ["GCP_TWOSIDED_NVL"] = "0"   # the NCCL send/recv two-sided path (twosided.cu)
+        mode = "twosided"
     mode = "sync" if mode == "sync32" else mode
     # TG, TE: the C18 bounds (gradient per element vs the rounding scale S, loss
     # estimate vs sum |terms|) from an identical state.  TM / TM_FIT / TE_FIT bound
@@ -105,6 +108,8 @@ def main():
     oe, sc = run.estimate(5, 1500, 1500)
     assert abs(est - oe) <= TE * sc, (est, oe)
     feats = ctx.dist_features()
+    if mode == "twosided":   # device-driven over NVLink windows unless GCP_TWOSIDED_NVL=0
+        assert feats["fused"] == (os.environ.get("GCP_TWOSIDED_NVL") != "0"), feats
     ctx.close()
 
     # the epoch loop (R20) on a side stream: the iterations of an epoch replay
