@@ -180,11 +180,7 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     s.keys = c->d_keys;
     s.err_slot = c->d_err;
     s.it_dev = nullptr;
-    s.ord_buf = nullptr;
-    s.ord_prefix = nullptr;
-    s.ord_ovf = nullptr;
-    s.ord_bits = 0;
-    s.ord_capbits = 0;
+    s.order = nullptr;
     if (c->capturing) {   // epoch graph: this launch's iteration relative to the replay's first
         s.it_dev = &c->d_step->it;
         s.it = it - c->graph_it0;
@@ -211,16 +207,15 @@ ModelArgs model_args(const gcp_ctx* c) {
 // the slot-order buffers (their table T is per tensor: dropped with the tensor)
 void ord_free(gcp_ctx* c) {
     graph_drop(c);
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     gfree(c, c->d_ord_buf);
     c->d_ord_buf = nullptr;
     c->d_ord_T = nullptr;
     c->d_ord_lut = nullptr;
     c->d_ord_cnt = nullptr;
-    for (int i = 0; i < 2; ++i) {
-        c->d_ord_bkt[i] = nullptr;
-        c->d_ord_ovf[i] = nullptr;
-    }
+    c->d_ord = nullptr;
+    c->d_ord_key = nullptr;
+    c->d_ord_rank = nullptr;
     c->ord_cap = 0;
 }
 
@@ -718,7 +713,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     c->t = 0;
     c->ts = 0;
     c->it = 0;
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     c->grad_blocks = sample_kernel_blocks(c);
     ST_TRY(ensure_partials(c, c->grad_blocks));
     c->have_model = true;
@@ -805,7 +800,7 @@ gcp_status gcp_sample(gcp_ctx* c, gcp_strategy strategy, int64_t s_nz, int64_t s
     c->q_w = q_w;
     c->seed = seed;
     c->bound = true;
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     graph_drop(c);
     return GCP_OK;
 }
@@ -873,7 +868,7 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     if (c->slot_order && !two_sided(c) && n_slots < ((int64_t)1 << 32)) {
         // group this iteration's slots by mode-1 position (same sample set, other
         // visiting order), so the K2 gathers / scatter-adds of one mode-1 row meet
-        // in L2 (kernels.cu launch_slot_order: hand-written bucket buffers + a scan)
+        // in L2 (kernels.cu launch_slot_order: hand-written histogram / scan / scatter)
         if (n_slots > c->ord_cap && !c->capturing) {
             ord_free(c);
             // a visiting-order optimisation only: without the memory for it, K2
@@ -888,18 +883,22 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
             }
         }
         if (c->slot_order && n_slots <= c->ord_cap) {
-            // the previous iteration's K2 may have carried this histogram
-            const bool done = c->ord_hist_ready && c->ord_hist_it == c->it;
-            prof_begin(c, PROF_OTHER, &ev);
-            CUDA_TRY(c, launch_slot_order(c, &so, done), "slot order");
-            prof_end(c, PROF_OTHER, ev);
+            // the previous iteration's K2 / Adam may have prepared this order
+            const int stage = c->ord_stage_it == c->it ? c->ord_stage : 0;
+            if (stage < 2) {
+                prof_begin(c, PROF_OTHER, &ev);
+                CUDA_TRY(c, launch_slot_order(c, s, &so.order, stage), "slot order");
+                prof_end(c, PROF_OTHER, ev);
+            } else {
+                so.order = c->d_ord;
+            }
         }
     }
-    c->ord_hist_ready = false;
+    c->ord_stage = 0;
     // the gradient K2 carries the next iteration's slot histogram
     OrdHistArgs oh;
     bool carry = false;
-    if (so.ord_buf) {
+    if (so.order) {
         const SampleArgs nx = sample_args(c, c->p_w, c->q_w, c->seed, c->it + 1, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
         carry = ord_hist_args(c, nx, &oh);
     }
@@ -909,8 +908,8 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
              "gcp_loss_grad");
     prof_end(c, PROF_GRAD, ev);
     if (carry) {
-        c->ord_hist_ready = true;
-        c->ord_hist_it = c->it + 1;
+        c->ord_stage = 1;
+        c->ord_stage_it = c->it + 1;
     }
     c->have_grad = true;
     if (with_loss) {
@@ -973,13 +972,25 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
         seg.len[0] = c->n_coef;
         seg.n = 1;
     }
+    // the next iteration's slot-order scan (launched here) and scatter (carried
+    // by this memory-bound Adam launch), when its histogram is ready
+    OrdScatterArgs os;
+    bool carry = false;
     cudaEvent_t ev;
+    if (c->ord_stage == 1 && c->ord_stage_it == c->it + 1) {
+        int64_t vecs = 0;
+        for (int i = 0; i < seg.n; ++i) vecs += seg.len[i] / (c->prec == GCP_FP32 ? 4 : 2);
+        prof_begin(c, PROF_OTHER, &ev);
+        carry = ord_scatter_args(c, c->p_w + c->q_w, &os, vecs);
+        prof_end(c, PROF_OTHER, ev);
+    }
     prof_begin(c, PROF_ADAM, &ev);
     CUDA_TRY(c, launch_adam(c, seg, c->d_A, c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2, p->eps, lower,
                             c->capturing ? c->t - c->graph_t0 : c->t, sharded ? 0 : 1, c->ag_stride,
-                            c->capturing ? c->d_step : nullptr),
+                            c->capturing ? c->d_step : nullptr, carry ? &os : nullptr),
              "gcp_adam_step");
     prof_end(c, PROF_ADAM, ev);
+    if (carry) c->ord_stage = 2;
     if (sharded) {
         CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, (size_t)c->n_coef * tsz(c), c->stream), "adam G reset");
         if (!two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // two-sided: rows stay partitioned

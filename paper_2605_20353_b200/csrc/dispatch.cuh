@@ -89,18 +89,20 @@ cudaError_t export_T(gcp_ctx* c, const SampleArgs& s, int64_t first, int64_t cou
 template <typename T>
 cudaError_t adam_T(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                    double beta1, double beta2, double eps, double lower, int64_t t, int zero_g, int R_pad,
-                   int row_stride, const DevStep* step) {
+                   int row_stride, const DevStep* step, const OrdScatterArgs* os) {
     const double bc1 = 1.0 / (1.0 - pow(beta1, (double)t));
     const double bc2 = 1.0 / (1.0 - pow(beta2, (double)t));
     int64_t nvec = 0;
     for (int i = 0; i < seg.n; ++i) nvec += seg.len[i] / Vec16<T>::n;
-    if (nvec == 0) return cudaSuccess;
-    int64_t nb = (nvec + 255) / 256;
+    OrdScatterArgs nos;
+    memset(&nos, 0, sizeof(nos));
+    if (nvec == 0 && !(os && os->n)) return cudaSuccess;
+    int64_t nb = (std::max<int64_t>(nvec, 1) + 255) / 256;
     const int64_t cap = (int64_t)c->sm_count * 8;
     if (nb > cap) nb = cap;
     k_adam<T><<<(int)nb, 256, 0, c->stream>>>(seg, nvec, (T*)A, (T*)G, (T*)B, (T*)C, (T)rate, (T)beta1,
                                               (T)beta2, (T)eps, (T)bc1, (T)bc2, (T)lower, zero_g, R_pad, row_stride, step,
-                                              (long long)t);
+                                              (long long)t, os ? *os : nos);
     return cudaGetLastError();
 }
 

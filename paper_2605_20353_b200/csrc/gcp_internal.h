@@ -54,14 +54,7 @@ struct SampleArgs {
     const uint32_t* it_dev;   // non-null inside a captured epoch graph: it = *it_dev + it (offset)
     const uint64_t* filter;   // blocked Bloom filter of the block's keys (4 u64 per 32-B sector), or null
     uint64_t filter_mask;     // sectors - 1 (power of two)
-    // gradient launches visiting the slots in mode-1 order (kernels.cu, slot
-    // order; ord_buf == null: slot order): position p -> bucket b (largest b
-    // with ord_prefix[b] <= p) -> slot ord_buf[(b << ord_capbits) + p -
-    // ord_prefix[b]]; positions past ord_prefix[2^bits] read the overflow list
-    const uint32_t* ord_buf;
-    const uint32_t* ord_prefix;
-    const uint32_t* ord_ovf;
-    int ord_bits, ord_capbits;
+    const uint32_t* order;    // gradient launches: slot processing order (null = slot order), see slot_order
 };
 
 // Epoch-graph replay state: the values of rate, t and it at the start of the
@@ -83,20 +76,28 @@ struct ModelArgs {
     int row_stride;           // elements between consecutive rows (R_pad, or 2 R_pad when A/G interleave)
 };
 
-// The slot-order histogram of the NEXT iteration, carried by the gradient K2
-// of this one (kernels.cu): slot s goes straight into its bucket's buffer at
-// the rank an atomicAdd on the bucket count returns (or, past the bucket
-// capacity, onto the overflow list).  n = 0 means none.
+// The slot-order histogram pass of the NEXT iteration, carried by the gradient
+// K2 of this one (kernels.cu, launch_slot_order): n = 0 means none.
 struct OrdHistArgs {
     SampleArgs sa;            // the next iteration's sampler arguments
     const uint16_t* lut;      // per-tensor lookup: bucket of nonzero index j = lut[j >> lut_shift]
     int lut_shift;
-    int bits, capbits;        // log2 bucket count, log2 bucket capacity
-    uint32_t* counts;         // per-bucket arrivals (zeroed by the scan)
-    uint32_t* buf;            // 2^bits x 2^capbits slot ids (this parity)
-    uint32_t* ovf;            // overflow slot ids (this parity)
-    uint32_t* novf;           // overflow count (this parity)
+    uint16_t* keys;           // bucket per slot (out)
+    uint32_t* ranks;          // rank of the slot inside its bucket (out)
+    uint32_t* totals;         // bucket totals (global atomicAdd)
+    int bits;                 // log2 bucket count
     int64_t n;                // slots (p + q)
+};
+
+// The scatter pass of the next iteration's slot order, carried by the Adam
+// launch of this one: order[cursor[key] + rank] = slot.  n = 0 means none.
+struct OrdScatterArgs {
+    const uint16_t* keys;
+    const uint32_t* ranks;
+    const uint32_t* cursor;
+    uint32_t* order;
+    int64_t n;
+    int ratio;                // one slot per `ratio` Adam vectors of a thread
 };
 
 struct Segment {              // contiguous ranges of the coefficient arrays (Adam)
@@ -205,16 +206,16 @@ struct gcp_ctx {
     // grouped by mode-1 position; one allocation (d_ord_buf) sized for ord_cap slots
     void* d_ord_buf = nullptr;
     int64_t* d_ord_T = nullptr;         // per-tensor bucket -> first record table (2^bits + 1)
-    uint16_t* d_ord_lut = nullptr;      // per-tensor nonzero index -> bucket lookup
+    uint16_t* d_ord_lut = nullptr;      // per-tensor nonzero index -> bucket lookup (kernels.cu)
     int ord_lut_shift = 0;
-    uint32_t* d_ord_cnt = nullptr;      // bucket counts (2^bits), prefix (2^bits + 1), overflow counts (2)
-    uint32_t* d_ord_bkt[2] = {nullptr, nullptr};   // per parity: bucket buffers (2^bits x 2^capbits)
-    uint32_t* d_ord_ovf[2] = {nullptr, nullptr};   // per parity: overflow lists (ord_cap)
+    uint32_t* d_ord_cnt = nullptr;      // bucket totals, cursors
+    uint32_t* d_ord = nullptr;          // visiting order (slot ids)
+    uint16_t* d_ord_key = nullptr;      // bucket per slot
+    uint32_t* d_ord_rank = nullptr;     // rank of the slot inside its bucket
     int64_t ord_cap = 0;
     int ord_bits = 15;                  // log2 of the bucket count (GCP_ORD_BITS)
-    int ord_capbits = 0;                // log2 of the bucket capacity
-    bool ord_hist_ready = false;        // the histogram of iteration ord_hist_it was carried by a K2
-    uint32_t ord_hist_it = 0;
+    int ord_stage = 0;                  // slot order of iteration ord_stage_it prepared by earlier launches:
+    uint32_t ord_stage_it = 0;          // 1 histogram (in K2), 2 scan + scatter too (in Adam), 0 nothing
     int slot_order = 0;                 // decided in gcp_model_init (GCP_SLOT_ORDER overrides)
     cudaGraphExec_t graph_exec = nullptr;
     double graph_key[8] = {0};
@@ -265,15 +266,17 @@ cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArg
                                  const OrdHistArgs* oh = nullptr);   // next iteration's slot histogram
 size_t slot_order_bytes(int64_t cap);
 cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap);   // carve buffers, build the per-tensor table
-cudaError_t launch_slot_order(gcp_ctx* c, SampleArgs* s, bool hist_done);   // sets s->ord_*
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, int stage);
 bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh);
+bool ord_scatter_args(gcp_ctx* c, int64_t n, OrdScatterArgs* os, int64_t adam_vecs);   // + launches the scan
 cudaError_t launch_reduce_partials(gcp_ctx* c, const double* partials, int n, double* out);
 cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t first, int64_t count,
                           const int64_t* lo, int64_t* subs, int64_t* j, int32_t* att);
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C,
                         double rate, double beta1, double beta2, double eps, double lower,
                         int64_t t, int zero_g, int row_stride = 0,    // row_stride 0: contiguous A/G
-                        const DevStep* step = nullptr);               // step: t = step->t + t (offset), rate
+                        const DevStep* step = nullptr,                // step: t = step->t + t (offset), rate
+                        const OrdScatterArgs* os = nullptr);          // fused next-iteration slot scatter
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff);
 cudaError_t launch_scale(gcp_ctx* c, void* x, int64_t n, double s);
 cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int64_t n);

@@ -18,9 +18,9 @@ cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int6
 cudaError_t export_f64(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
                        int32_t*);
 cudaError_t adam_f32(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int, const DevStep*);
+                     double, int64_t, int, int, int, const DevStep*, const OrdScatterArgs*);
 cudaError_t adam_f64(gcp_ctx*, const Segment&, void*, void*, void*, void*, double, double, double, double,
-                     double, int64_t, int, int, int, const DevStep*);
+                     double, int64_t, int, int, int, const DevStep*, const OrdScatterArgs*);
 cudaError_t init_f32(gcp_ctx*, const InitArgs&, void*);
 cudaError_t init_f64(gcp_ctx*, const InitArgs&, void*);
 
@@ -46,11 +46,11 @@ cudaError_t launch_export(gcp_ctx* c, const SampleArgs& s, int stratum, int64_t 
 
 cudaError_t launch_adam(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                         double beta1, double beta2, double eps, double lower, int64_t t, int zero_g,
-                        int row_stride, const DevStep* step) {
+                        int row_stride, const DevStep* step, const OrdScatterArgs* os) {
     const int rs = row_stride > 0 ? row_stride : c->R_pad;
     return c->prec == GCP_FP32
-               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step)
-               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step);
+               ? adam_f32(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, os)
+               : adam_f64(c, seg, A, G, B, C, rate, beta1, beta2, eps, lower, t, zero_g, c->R_pad, rs, step, os);
 }
 
 cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
@@ -67,31 +67,28 @@ cudaError_t launch_init(gcp_ctx* c, uint64_t seed, const int64_t* goff) {
     return c->prec == GCP_FP32 ? init_f32(c, ia, c->d_A) : init_f64(c, ia, c->d_A);
 }
 
-// Slot ordering for the gradient K2 (DRAM-resident mode-1 rows: c4, c5): the
-// iteration's slots grouped into 2^bits buckets of mode-1 position (default
-// 2^15), nonzero and zero slots interleaved (a bucket holds the nonzero slots
-// whose record lies in a mode-1 row range AND the zero slots whose attempt-0
-// candidate lies in the same range, so K2 fills the A|G lines of a row range
-// once per iteration, not once per stratum).  The sample set, and so the
-// estimate, is unchanged; only the visiting order changes, so that K2's
-// gathers and scatter-adds of one mode-1 row meet in L2 and its DRAM accesses
-// walk the records and rows forward.
-//   histogram   per slot: Philox word -> bucket (kernels.cuh ord_bucket); the
-//               slot id goes straight into the bucket's fixed-capacity buffer at
-//               the rank an atomicAdd on the bucket count returns (overflow list
-//               past the capacity).  Carried by the previous iteration's
-//               gradient K2 (OrdHistArgs: ALU work and scattered 4-B stores
-//               under its memory-bound gathers), else k_ord_hist.
-//   k_ord_scan  one CTA: exclusive prefix of min(count, capacity) -> the visiting
-//               order's bucket offsets; counts and the next parity's overflow
-//               count reset
-//   K2          position p -> bucket (binary search of the prefix, L1-resident)
-//               -> slot id in the bucket buffer (kernels.cuh slot_at)
-// No scatter pass: a bucket buffer is read where the histogram wrote it.  The
-// buffers are double-buffered by iteration parity (K2 of t reads parity t while
-// it fills parity t+1).  Order inside a bucket is the atomics' arrival order
-// (run to run it varies), which only moves the fp32 atomic summation order of K2.
-constexpr int kOrdMaxBits = 15;            // counter / table capacity
+// Slot ordering for the gradient K2 (DRAM-resident mode-1 rows: c4, c5): a
+// hand-written counting sort of the iteration's slots into 2^bits buckets of
+// mode-1 position (default 2^15), nonzero and zero slots interleaved (a bucket
+// holds the nonzero slots whose record lies in a mode-1 row range AND the zero
+// slots whose attempt-0 candidate lies in the same range, so K2 fills the A|G
+// lines of a row range once per iteration, not once per stratum).  The sample
+// set, and so the estimate, is unchanged; only the visiting order changes, so
+// that K2's gathers and scatter-adds of one mode-1 row meet in L2 and its DRAM
+// accesses walk the records and rows forward.
+//   histogram      per slot: Philox word -> bucket (kernels.cuh ord_bucket) and
+//                  the slot's rank inside its bucket (a global atomicAdd);
+//                  carried by the previous iteration's gradient K2 (OrdHistArgs:
+//                  ALU work under its memory-bound gathers), else k_ord_hist
+//   k_ord_scan     one CTA: exclusive scan of the bucket totals -> cursors;
+//                  totals reset for the next iteration
+//   k_ord_scatter  order[cursor[bucket] + rank] = slot (GCP_ORD_FUSE=2 carries
+//                  it in the previous Adam launch instead: slower, see
+//                  ord_scatter_args)
+// So in steady state an iteration launches the scan and the scatter.
+// Order inside a bucket is the atomics' arrival order (run to run it varies),
+// which only moves the fp32 atomic summation order of K2.
+constexpr int kOrdMaxBits = 15;            // table / counter capacity
 constexpr int kOrdThreads = 1024;
 constexpr int kOrdLutBits = 20;            // nonzero-index lookup cells (u16 each: 2 MB, L2-resident)
 
@@ -100,15 +97,6 @@ int ord_bits_env() {
     const char* e = getenv("GCP_ORD_BITS");
     const int b = e ? atoi(e) : 15;
     return b < 10 ? 10 : (b > kOrdMaxBits ? kOrdMaxBits : b);
-}
-
-// bucket capacity 2^capbits: >= 2.5x the mean bucket load (the overflow list
-// takes the rest)
-static int ord_capbits_for(int64_t cap, int bits) {
-    const double mean = (double)cap / (double)(1 << bits);
-    int cb = 4;
-    while ((double)(1 << cb) < 2.5 * mean && cb < 24) ++cb;
-    return cb;
 }
 
 // T[b] = first canonical record whose c_1 >= ceil(b I_1 / B), b = 0..B (T[B] = N):
@@ -143,8 +131,9 @@ __global__ void k_ord_lut(const int64_t* __restrict__ T, int bits, int shift, in
     }
 }
 
-// Histogram for an iteration whose histogram no gradient K2 carried (the first
-// of an epoch graph, eager calls): four slots per thread in flight.
+// Histogram pass for an iteration whose histogram no gradient K2 computed (the
+// first of an epoch graph, eager calls):
+// bucket and in-bucket rank of every slot, four slots per thread in flight.
 __global__ void __launch_bounds__(256) k_ord_hist(const OrdHistArgs oh) {
     const uint32_t it = iter_word(oh.sa);
     const uint64_t inv = oh.sa.bdim[0] > 1 ? (~0ull) / oh.sa.bdim[0] : 0;
@@ -156,20 +145,18 @@ __global__ void __launch_bounds__(256) k_ord_hist(const OrdHistArgs oh) {
     }
 }
 
-// one CTA: prefix[b] = sum_{b' < b} min(count[b'], capacity), prefix[B] = the
-// slots in buckets; counts reset, the next parity's overflow count reset.  The
-// counts pass through shared memory with one pad word per 32 (conflict-free
+// one CTA: exclusive scan of the bucket totals -> cursors; totals reset.  The
+// totals pass through shared memory with one pad word per 32 (conflict-free
 // per-thread segments).
-__global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__ counts, uint32_t* __restrict__ prefix,
-                                                         uint32_t* __restrict__ novf_next, int B, uint32_t capacity) {
+__global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__ totals, uint32_t* __restrict__ cursor,
+                                                         int B) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
     uint32_t* sv = reinterpret_cast<uint32_t*>(ord_smem);   // B + B/32 words
     __shared__ uint32_t wsum[kOrdThreads / 32];
     for (int i = threadIdx.x; i < B; i += kOrdThreads) {
-        sv[i + (i >> 5)] = min(counts[i], capacity);
-        counts[i] = 0;
+        sv[i + (i >> 5)] = totals[i];
+        totals[i] = 0;
     }
-    if (threadIdx.x == 0) *novf_next = 0;
     __syncthreads();
     const int per = B / kOrdThreads;   // B >= 2^10
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -203,9 +190,17 @@ __global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__
         sv[x + (x >> 5)] = base;
         base += v;
     }
-    if (t == kOrdThreads - 1) prefix[B] = base;
     __syncthreads();
-    for (int i = threadIdx.x; i < B; i += kOrdThreads) prefix[i] = sv[i + (i >> 5)];
+    for (int i = threadIdx.x; i < B; i += kOrdThreads) cursor[i] = sv[i + (i >> 5)];
+}
+
+// order[cursor[bucket] + rank] = slot: one pass, no atomics
+__global__ void __launch_bounds__(256) k_ord_scatter(const uint16_t* __restrict__ keys,
+                                                    const uint32_t* __restrict__ ranks, int64_t n,
+                                                    const uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += nt)
+        order[__ldg(cursor + keys[s]) + ranks[s]] = (uint32_t)s;
 }
 
 static int64_t lut_cells(int64_t N, int* shift) {
@@ -215,44 +210,32 @@ static int64_t lut_cells(int64_t N, int* shift) {
     return ((std::max<int64_t>(N, 1) - 1) >> sh) + 1;
 }
 
-// layout of the one slot-order allocation for cap slots (and the bucket bits)
-struct OrdLayout {
-    size_t T, lut, cnt, bkt[2], ovf[2], total;
-};
-static OrdLayout ord_layout(int64_t cap, int bits) {
+size_t slot_order_bytes(int64_t cap) {
     constexpr int B = 1 << kOrdMaxBits;
-    const int cb = ord_capbits_for(cap, bits);
     const size_t capr = (size_t)(cap + 15) / 16 * 16;
-    const size_t bk = ((size_t)1 << bits) << cb;
-    OrdLayout L;
-    size_t o = 0;
-    L.T = o;   o += (size_t)(B + 2) * sizeof(int64_t);
-    L.lut = o; o += ((size_t)1 << kOrdLutBits) * sizeof(uint16_t);
-    L.cnt = o; o += (size_t)(2 * B + 16) * sizeof(uint32_t);   // counts, prefix (B + 1), overflow counts
-    for (int i = 0; i < 2; ++i) { L.bkt[i] = o; o += bk * sizeof(uint32_t); }
-    for (int i = 0; i < 2; ++i) { L.ovf[i] = o; o += capr * sizeof(uint32_t); }
-    L.total = o + 256;
-    return L;
+    return capr * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * B * sizeof(uint32_t) + (B + 2) * sizeof(int64_t) +
+           ((size_t)1 << kOrdLutBits) * sizeof(uint16_t) + 256;
 }
-
-size_t slot_order_bytes(int64_t cap) { return ord_layout(cap, ord_bits_env()).total; }
 
 // Carve the order buffers out of one allocation of slot_order_bytes(cap) and
 // build the per-tensor tables T and lut (once per tensor).
 cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap) {
     constexpr int B = 1 << kOrdMaxBits;
+    const size_t capr = (size_t)(cap + 15) / 16 * 16;
     c->ord_bits = ord_bits_env();
-    c->ord_capbits = ord_capbits_for(cap, c->ord_bits);
-    const OrdLayout L = ord_layout(cap, c->ord_bits);
     char* p = static_cast<char*>(buf);
-    c->d_ord_T = reinterpret_cast<int64_t*>(p + L.T);
-    c->d_ord_lut = reinterpret_cast<uint16_t*>(p + L.lut);
-    c->d_ord_cnt = reinterpret_cast<uint32_t*>(p + L.cnt);
-    for (int i = 0; i < 2; ++i) {
-        c->d_ord_bkt[i] = reinterpret_cast<uint32_t*>(p + L.bkt[i]);
-        c->d_ord_ovf[i] = reinterpret_cast<uint32_t*>(p + L.ovf[i]);
-    }
-    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, (size_t)(2 * B + 16) * sizeof(uint32_t), c->stream);
+    c->d_ord_T = reinterpret_cast<int64_t*>(p);
+    p += (B + 2) * sizeof(int64_t);
+    c->d_ord_cnt = reinterpret_cast<uint32_t*>(p);
+    p += 2 * B * sizeof(uint32_t);
+    c->d_ord = reinterpret_cast<uint32_t*>(p);
+    p += capr * sizeof(uint32_t);
+    c->d_ord_rank = reinterpret_cast<uint32_t*>(p);
+    p += capr * sizeof(uint32_t);
+    c->d_ord_key = reinterpret_cast<uint16_t*>(p);
+    p += capr * sizeof(uint16_t);
+    c->d_ord_lut = reinterpret_cast<uint16_t*>(p);
+    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, 2 * B * sizeof(uint32_t), c->stream);
     if (e != cudaSuccess) return e;
     k_ord_table<<<((1 << c->ord_bits) + 1 + 255) / 256, 256, 0, c->stream>>>(
         c->d_rec, c->rec_words, c->val_words, c->N, (uint32_t)(c->hi[0] - c->lo[0]), c->ord_bits, c->d_ord_T);
@@ -263,36 +246,20 @@ cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap) {
     return cudaGetLastError();
 }
 
-static uint32_t* ord_prefix(gcp_ctx* c) { return c->d_ord_cnt + (1 << kOrdMaxBits); }
-static uint32_t* ord_novf(gcp_ctx* c, int par) { return c->d_ord_cnt + 2 * (1 << kOrdMaxBits) + 4 + par; }
-
-static OrdHistArgs make_hist_args(gcp_ctx* c, const SampleArgs& sa, int par) {
+static OrdHistArgs make_hist_args(gcp_ctx* c, const SampleArgs& sa) {
     OrdHistArgs oh;
     oh.sa = sa;
     oh.lut = c->d_ord_lut;
     oh.lut_shift = c->ord_lut_shift;
+    oh.keys = c->d_ord_key;
+    oh.ranks = c->d_ord_rank;
+    oh.totals = c->d_ord_cnt;
     oh.bits = c->ord_bits;
-    oh.capbits = c->ord_capbits;
-    oh.counts = c->d_ord_cnt;
-    oh.buf = c->d_ord_bkt[par];
-    oh.ovf = c->d_ord_ovf[par];
-    oh.novf = ord_novf(c, par);
     oh.n = sa.p + sa.q;
     return oh;
 }
 
-// The visiting order of this iteration (parity it & 1): its histogram unless
-// the previous gradient K2 carried it, then the scan; sets s->ord_*.
-cudaError_t launch_slot_order(gcp_ctx* c, SampleArgs* s, bool hist_done) {
-    const int64_t n = s->p + s->q;
-    const int par = (int)(c->it & 1);
-    const int B = 1 << c->ord_bits;
-    s->ord_buf = c->d_ord_bkt[par];
-    s->ord_prefix = ord_prefix(c);
-    s->ord_ovf = c->d_ord_ovf[par];
-    s->ord_bits = c->ord_bits;
-    s->ord_capbits = c->ord_capbits;
-    if (n == 0) return cudaSuccess;
+static cudaError_t ord_scan(gcp_ctx* c) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_ord_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -300,31 +267,67 @@ cudaError_t launch_slot_order(gcp_ctx* c, SampleArgs* s, bool hist_done) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    if (!hist_done) {
-        // counts may hold an unconsumed histogram (a K2 prepared an iteration
-        // that did not follow): start from zero
-        cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, (size_t)B * sizeof(uint32_t), c->stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(ord_novf(c, par), 0, sizeof(uint32_t), c->stream);
-        if (e != cudaSuccess) return e;
-        const int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
-        k_ord_hist<<<nb, 256, 0, c->stream>>>(make_hist_args(c, *s, par));
-        c->launches++;
-    }
-    k_ord_scan<<<1, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(c->d_ord_cnt, ord_prefix(c),
-                                                                        ord_novf(c, par ^ 1), B,
-                                                                        1u << c->ord_capbits);
+    const int B = 1 << c->ord_bits;
+    k_ord_scan<<<1, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(c->d_ord_cnt, c->d_ord_cnt + (1 << kOrdMaxBits),
+                                                                        B);
     c->launches++;
     return cudaGetLastError();
 }
 
-// The histogram of the next iteration (parity (it + 1) & 1) for the gradient
-// K2 to carry (GCP_ORD_FUSE=0 keeps it a launch of its own).
+// The order of this iteration's slots, from whatever the previous launches
+// prepared: stage 2 = nothing left, 1 = scan + scatter, 0 = everything.
+cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** order_out, int stage) {
+    const int64_t n = s.p + s.q;
+    *order_out = c->d_ord;
+    if (n == 0 || stage >= 2) return cudaSuccess;
+    const int B = 1 << c->ord_bits;
+    uint32_t* totals = c->d_ord_cnt;
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+    if (stage < 1) {
+        // totals may hold an unconsumed histogram (a K2 prepared an iteration
+        // that did not follow): start from zero
+        cudaError_t e = cudaMemsetAsync(totals, 0, (size_t)B * sizeof(uint32_t), c->stream);
+        if (e != cudaSuccess) return e;
+        k_ord_hist<<<nb, 256, 0, c->stream>>>(make_hist_args(c, s));
+        c->launches++;
+    }
+    cudaError_t e = ord_scan(c);
+    if (e != cudaSuccess) return e;
+    k_ord_scatter<<<nb, 256, 0, c->stream>>>(c->d_ord_key, c->d_ord_rank, n, c->d_ord_cnt + (1 << kOrdMaxBits),
+                                             c->d_ord);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+// The histogram of the next iteration for the gradient K2 to carry
+// (GCP_ORD_FUSE=0 keeps every pass a launch of its own; the histogram's Philox
+// and table lookups cost K2 nothing measurable on c4).
 bool ord_hist_args(gcp_ctx* c, const SampleArgs& next, OrdHistArgs* oh) {
     const char* fe = getenv("GCP_ORD_FUSE");
-    if ((fe && atoi(fe) == 0) || !c->d_ord_buf) return false;
+    if ((fe && atoi(fe) == 0) || !c->d_ord) return false;
     const int64_t n = next.p + next.q;
     if (n == 0 || n > c->ord_cap) return false;
-    *oh = make_hist_args(c, next, (int)((c->it + 1) & 1));
+    *oh = make_hist_args(c, next);
+    return true;
+}
+
+// The scan of the next iteration (launched here) and its scatter for the Adam
+// launch to carry -- only with GCP_ORD_FUSE=2: the random 4-B stores slowed
+// Adam's stream by more than the scatter launch costs (c4: Adam 0.70 -> 1.07 ms
+// against a 0.2-ms scatter).  Writing the slot ids straight into fixed-capacity
+// bucket buffers from the K2 histogram (no scatter pass at all) cost K2 the same
+// 0.2 ms of random 4-B stores (profiles/r02_summary.md).
+bool ord_scatter_args(gcp_ctx* c, int64_t n, OrdScatterArgs* os, int64_t adam_vecs) {
+    const char* fe = getenv("GCP_ORD_FUSE");
+    if (!(fe && atoi(fe) == 2)) return false;
+    if (!c->d_ord || n == 0 || n > c->ord_cap) return false;
+    if (ord_scan(c) != cudaSuccess) return false;
+    os->keys = c->d_ord_key;
+    os->ranks = c->d_ord_rank;
+    os->cursor = c->d_ord_cnt + (1 << kOrdMaxBits);
+    os->order = c->d_ord;
+    os->n = n;
+    os->ratio = (int)std::max<int64_t>(1, adam_vecs / n);
     return true;
 }
 

@@ -75,13 +75,12 @@ __device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16
     return (uint32_t)q;
 }
 
-// slot s into its bucket's buffer at the rank its count's atomicAdd returns;
-// past the bucket capacity onto the overflow list (visited last)
+// bucket of slot s and its rank inside the bucket (arrival order of a global
+// atomicAdd: the scatter then needs no reservation pass)
 __device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, uint32_t it, uint64_t inv) {
     const uint32_t b = ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
-    const uint32_t r = atomicAdd(oh.counts + b, 1u);
-    if (r < (1u << oh.capbits)) oh.buf[((size_t)b << oh.capbits) + r] = (uint32_t)s;
-    else oh.ovf[atomicAdd(oh.novf, 1u)] = (uint32_t)s;
+    oh.keys[s] = (uint16_t)b;
+    oh.ranks[s] = atomicAdd(oh.totals + b, 1u);
 }
 
 // One warp takes 32 consecutive slots: each lane draws one sample (index work
@@ -99,23 +98,9 @@ template <int D, int NV> struct SampleGeom {
     static constexpr int rowregs = small ? 4 : kRowRegBudget;
 };
 
-// position p of the visiting order -> slot (identity unless a slot order is
-// given): the bucket holding p by a binary search of the bucket prefix sums
-// (an L1-resident table), then the bucket's buffer; past the last bucket the
-// overflow list
-__device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t p, int64_t total) {
-    if (!a.ord_buf || p >= total) return p;
-    const uint32_t nb = 1u << a.ord_bits;
-    const uint32_t pp = (uint32_t)p;
-    const uint32_t in_buckets = __ldg(a.ord_prefix + nb);
-    if (pp >= in_buckets) return (int64_t)__ldg(a.ord_ovf + (pp - in_buckets));
-    uint32_t lo = 0, hi = nb;   // largest b with prefix[b] <= p
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(a.ord_prefix + mid) <= pp) lo = mid;
-        else hi = mid;
-    }
-    return (int64_t)__ldg(a.ord_buf + ((size_t)lo << a.ord_capbits) + (pp - __ldg(a.ord_prefix + lo)));
+// position s of the visiting order -> slot (identity unless a slot order is given)
+__device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t s, int64_t total) {
+    return (a.order && s < total) ? (int64_t)__ldg(a.order + s) : s;
 }
 
 template <typename T, int D, int GL, int NV>
@@ -279,11 +264,11 @@ __global__ void k_export(const SampleArgs sa, int64_t first, int64_t count, cons
 // B <- b1 B + (1-b1) g; C <- b2 C + (1-b2) g^2; A <- A - rate (B bc1)/sqrt(C bc2 + eps);
 // A <- (A < l) ? l : A; G <- 0 (fused reset).  bc = 1/(1-beta^t) from the host in fp64.
 template <typename T>
-__global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) k_adam(const Segment seg, int64_t nvec_total, T* __restrict__ A,
                                               T* __restrict__ G, T* __restrict__ B, T* __restrict__ C,
                                               T rate, T b1, T b2, T eps, T bc1, T bc2, T lower,
                                               int zero_g, int R_pad, int row_stride, const DevStep* step,
-                                              long long t_off) {
+                                              long long t_off, const OrdScatterArgs os) {
     using V = typename Vec16<T>::type;
     constexpr int VE = Vec16<T>::n;
     if (step) {   // graph replay: t = t0 + offset, bias corrections in fp64 from it
@@ -292,8 +277,17 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
         bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
         bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec_total;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    // the next iteration's slot-order scatter (random 4-B stores into L2)
+    // interleaved with this memory-bound stream, one slot per os.ratio vectors
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    int64_t hs = tid;
+    int hstep = 0;
+    for (int64_t i = tid; i < nvec_total; i += nt) {
+        if (hs < os.n && ++hstep == os.ratio) {
+            hstep = 0;
+            os.order[__ldg(os.cursor + os.keys[hs]) + os.ranks[hs]] = (uint32_t)hs;
+            hs += nt;
+        }
         // map the virtual vector index onto its segment
         int64_t rem = i;
         int sidx = 0;
@@ -327,6 +321,7 @@ __global__ void __launch_bounds__(256) k_adam(const Segment seg, int64_t nvec_to
             *reinterpret_cast<V*>(G + ea) = z;
         }
     }
+    for (; hs < os.n; hs += nt) os.order[__ldg(os.cursor + os.keys[hs]) + os.ranks[hs]] = (uint32_t)hs;
 }
 
 struct InitArgs {

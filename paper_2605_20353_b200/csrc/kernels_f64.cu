@@ -14,8 +14,8 @@ cudaError_t export_f64(gcp_ctx* c, const SampleArgs& s, int64_t first, int64_t c
 }
 cudaError_t adam_f64(gcp_ctx* c, const Segment& seg, void* A, void* G, void* B, void* C, double rate,
                    double b1, double b2, double eps, double lower, int64_t t, int zero_g, int R_pad,
-                   int row_stride, const DevStep* step) {
-    return adam_T<double>(c, seg, A, G, B, C, rate, b1, b2, eps, lower, t, zero_g, R_pad, row_stride, step);
+                   int row_stride, const DevStep* step, const OrdScatterArgs* os) {
+    return adam_T<double>(c, seg, A, G, B, C, rate, b1, b2, eps, lower, t, zero_g, R_pad, row_stride, step, os);
 }
 cudaError_t init_f64(gcp_ctx* c, const InitArgs& ia, void* A) { return init_T<double>(c, ia, A); }
 }  // namespace gcp
