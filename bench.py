@@ -346,6 +346,12 @@ def main():
     elif w["nnz"] > 3_000_000_000:
         # c5 at one GPU: its 150 GB int64 + fp64 COO exceeds the device, so the
         # generator hands each finished partition to host memory
+        import psutil
+        need = w["nnz"] * 1.006 * (8 * w["d"] + 8) + 8e9
+        avail = psutil.virtual_memory().available
+        if avail < need:
+            raise SystemExit(f"bench: {name} at one GPU needs ~{need / 1e9:.0f} GB of host memory for its COO, "
+                             f"{avail / 1e9:.0f} GB available")
         subs, vals, gen_s = make_tensor(name, f"cuda:{dev}", out_device="cpu")
         host_gen = True
         args.no_e2e = True
