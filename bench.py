@@ -339,22 +339,26 @@ def main():
 
     log("generate", name)
     host_gen = False
+    # a rank block beyond 1.5e9 nonzeros (c5 at 1-2 GPUs: 75-150 GB of int64 +
+    # fp64 COO) does not fit the device beside its ingest: the generator hands
+    # each finished partition to host memory and the ingest reads it from there
+    blk_nnz = w["nnz"] / ws
+    if blk_nnz > 1_500_000_000:
+        import psutil
+        need = blk_nnz * 1.006 * (8 * w["d"] + 8) * (ws if ws > 1 else 1) + 8e9
+        avail = psutil.virtual_memory().available
+        if avail < need:
+            raise SystemExit(f"bench: {name} at {ws} GPU(s) needs ~{need / 1e9:.0f} GB of host memory for its COO, "
+                             f"{avail / 1e9:.0f} GB available")
+        host_gen = True
+        args.no_e2e = True
     if ws > 1 and w["nnz"] > 1_000_000_000:
         # billion-scale: each rank generates only its block of the global tensor
         subs, vals, gen_s = make_tensor(name, f"cuda:{dev}", block=(lo[rank], hi[rank]),
-                                        allreduce=lambda x: allsum_int(ws, x))
-    elif w["nnz"] > 3_000_000_000:
-        # c5 at one GPU: its 150 GB int64 + fp64 COO exceeds the device, so the
-        # generator hands each finished partition to host memory
-        import psutil
-        need = w["nnz"] * 1.006 * (8 * w["d"] + 8) + 8e9
-        avail = psutil.virtual_memory().available
-        if avail < need:
-            raise SystemExit(f"bench: {name} at one GPU needs ~{need / 1e9:.0f} GB of host memory for its COO, "
-                             f"{avail / 1e9:.0f} GB available")
+                                        allreduce=lambda x: allsum_int(ws, x),
+                                        out_device="cpu" if host_gen else None)
+    elif host_gen:
         subs, vals, gen_s = make_tensor(name, f"cuda:{dev}", out_device="cpu")
-        host_gen = True
-        args.no_e2e = True
     else:
         subs, vals, gen_s = make_tensor(name, f"cuda:{dev}")
         if ws > 1:

@@ -282,7 +282,8 @@ gcp_status gcp_fit(gcp_ctx* ctx, const gcp_fit_params* p, gcp_trace_fn trace, vo
 
 /* Layout choices the context made (all nullable; 0 without a model / tensor):
  * A/G rows interleaved in one 128-B line (factors spill L2), gradient slots
- * visited in mode-1 order (mode-1 rows spill L2; kernels.cu), L2 Bloom filter
+ * visited in mode-1 order (mode-1 rows spill L2 and the iteration's order array
+ * fits L2; kernels.cu), L2 Bloom filter
  * in front of the zero test.  For tests and benchmarks.  Does not block. */
 gcp_status gcp_layout(gcp_ctx* ctx, int* ag_interleaved, int* slot_order, int* filter);
 

@@ -651,9 +651,13 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         c->ag_stride = il ? 2 * c->R_pad : c->R_pad;
         // slot ordering by mode-1 position: pays when mode 1's A and G rows
         // themselves spill out of L2 (c4, c5); GCP_SLOT_ORDER=0/1 overrides
+        // (and, decided per iteration in gcp_loss_grad, when the order array of
+        // the iteration's slots fits L2: c5's 2e8 slots ordered cost more than
+        // they saved, profiles/r02_summary.md)
         const char* oenv = getenv("GCP_SLOT_ORDER");
         const bool m1_spills = 2.0 * (double)c->rows[0] * (double)rb > 0.25 * (double)c->l2_bytes;
         c->slot_order = oenv ? atoi(oenv) != 0 : m1_spills;
+        c->slot_order_forced = oenv && atoi(oenv) != 0;
     }
     const size_t bytes = (size_t)std::max<int64_t>(c->n_coef, 4) * tsz(c);
     // sync: the fused NVLink exchange; two-sided: the device-driven import /
@@ -865,7 +869,8 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     SampleArgs so = s;
     // slot ids are u32: beyond 2^32 slots per rank K2 runs in slot order
     const int64_t n_slots = c->p_w + c->q_w;
-    if (c->slot_order && !two_sided(c) && n_slots < ((int64_t)1 << 32)) {
+    const bool order_fits = c->slot_order_forced || (double)n_slots * 4.0 <= 0.8 * (double)c->l2_bytes;
+    if (c->slot_order && !two_sided(c) && n_slots < ((int64_t)1 << 32) && order_fits) {
         // group this iteration's slots by mode-1 position (same sample set, other
         // visiting order), so the K2 gathers / scatter-adds of one mode-1 row meet
         // in L2 (kernels.cu launch_slot_order: hand-written histogram / scan / scatter)
@@ -1202,7 +1207,9 @@ gcp_status gcp_dist_features(gcp_ctx* c, int* fused_out, int* multimem_out) {
 gcp_status gcp_layout(gcp_ctx* c, int* ag_interleaved, int* slot_order, int* filter) {
     ENTER(c);
     if (ag_interleaved) *ag_interleaved = c->have_model && c->ag_interleaved ? 1 : 0;
-    if (slot_order) *slot_order = c->have_model && c->slot_order ? 1 : 0;
+    const bool order_fits = c->slot_order_forced || !c->bound ||
+                            (double)(c->p_w + c->q_w) * 4.0 <= 0.8 * (double)c->l2_bytes;
+    if (slot_order) *slot_order = c->have_model && c->slot_order && order_fits && !two_sided(c) ? 1 : 0;
     if (filter) *filter = c->have_tensor && c->filter_sectors ? 1 : 0;
     return GCP_OK;
 }

@@ -82,7 +82,8 @@ struct OrdHistArgs {
     SampleArgs sa;            // the next iteration's sampler arguments
     const uint16_t* lut;      // per-tensor lookup: bucket of nonzero index j = lut[j >> lut_shift]
     int lut_shift;
-    uint16_t* keys;           // bucket per slot (out)
+    uint32_t* keys;           // (tile << bits) | bucket per slot (out)
+    int tile_shift;           // slots per tile = 2^tile_shift (tiles order independently)
     uint32_t* ranks;          // rank of the slot inside its bucket (out)
     uint32_t* totals;         // bucket totals (global atomicAdd)
     int bits;                 // log2 bucket count
@@ -92,7 +93,7 @@ struct OrdHistArgs {
 // The scatter pass of the next iteration's slot order, carried by the Adam
 // launch of this one: order[cursor[key] + rank] = slot.  n = 0 means none.
 struct OrdScatterArgs {
-    const uint16_t* keys;
+    const uint32_t* keys;
     const uint32_t* ranks;
     const uint32_t* cursor;
     uint32_t* order;
@@ -210,13 +211,15 @@ struct gcp_ctx {
     int ord_lut_shift = 0;
     uint32_t* d_ord_cnt = nullptr;      // bucket totals, cursors
     uint32_t* d_ord = nullptr;          // visiting order (slot ids)
-    uint16_t* d_ord_key = nullptr;      // bucket per slot
+    uint32_t* d_ord_key = nullptr;      // (tile, bucket) per slot
+    int ord_tile_shift = 62, ord_ntiles = 1;   // slot tiles ordered independently (large p + q)
     uint32_t* d_ord_rank = nullptr;     // rank of the slot inside its bucket
     int64_t ord_cap = 0;
     int ord_bits = 15;                  // log2 of the bucket count (GCP_ORD_BITS)
     int ord_stage = 0;                  // slot order of iteration ord_stage_it prepared by earlier launches:
     uint32_t ord_stage_it = 0;          // 1 histogram (in K2), 2 scan + scatter too (in Adam), 0 nothing
     int slot_order = 0;                 // decided in gcp_model_init (GCP_SLOT_ORDER overrides)
+    bool slot_order_forced = false;     // GCP_SLOT_ORDER=1: also when the order array does not fit L2
     cudaGraphExec_t graph_exec = nullptr;
     double graph_key[8] = {0};
     double graph_seen[8] = {0};         // key of the last eager epoch: capture on the second sighting

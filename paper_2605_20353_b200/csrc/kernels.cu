@@ -149,7 +149,11 @@ __global__ void __launch_bounds__(256) k_ord_hist(const OrdHistArgs oh) {
 // totals pass through shared memory with one pad word per 32 (conflict-free
 // per-thread segments).
 __global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__ totals, uint32_t* __restrict__ cursor,
-                                                         int B) {
+                                                         int B, int tile_shift) {
+    // CTA t scans tile t's buckets; tile t's slots fill order[t << tile_shift, ...)
+    totals += (size_t)blockIdx.x * B;
+    cursor += (size_t)blockIdx.x * B;
+    const uint32_t tile_base = tile_shift < 32 ? (uint32_t)blockIdx.x << tile_shift : 0u;
     extern __shared__ __align__(16) unsigned char ord_smem[];
     uint32_t* sv = reinterpret_cast<uint32_t*>(ord_smem);   // B + B/32 words
     __shared__ uint32_t wsum[kOrdThreads / 32];
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__
         if (lane < kOrdThreads / 32) wsum[lane] = xi - x;   // exclusive prefix of the warp totals
     }
     __syncthreads();
-    uint32_t base = wsum[w] + incl - run;
+    uint32_t base = tile_base + wsum[w] + incl - run;
     for (int i = 0; i < per; ++i) {
         const int x = t * per + i;
         const uint32_t v = sv[x + (x >> 5)];
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_ord_scan(uint32_t* __restrict__
 }
 
 // order[cursor[bucket] + rank] = slot: one pass, no atomics
-__global__ void __launch_bounds__(256) k_ord_scatter(const uint16_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) k_ord_scatter(const uint32_t* __restrict__ keys,
                                                     const uint32_t* __restrict__ ranks, int64_t n,
                                                     const uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
@@ -210,11 +214,28 @@ static int64_t lut_cells(int64_t N, int* shift) {
     return ((std::max<int64_t>(N, 1) - 1) >> sh) + 1;
 }
 
+// Large p + q (c5 at one GPU: 2e8 slots, an 800-MB order array) are ordered in
+// independent tiles of consecutive slots whose order regions fit L2, so the
+// scatter's random stores stay in L2 (an order array spilling to DRAM turns
+// every 4-B store into a sector read-modify-write); K2 then visits the tiles
+// one after the other, each in mode-1 order.  GCP_ORD_TILE_MB (default 128)
+// bounds a tile's order region.
+static constexpr int kOrdMaxTiles = 64;
+static int ord_tile_shift_for(int64_t cap) {
+    const char* e = getenv("GCP_ORD_TILE_MB");
+    const double mb = e && atof(e) > 0 ? atof(e) : 128.0;
+    if ((double)cap * 4.0 <= mb * 1048576.0 * 1.25) return 62;   // one tile
+    int sh = 10;
+    while ((double)((int64_t)1 << (sh + 1)) * 4.0 <= mb * 1048576.0) ++sh;
+    while (((cap + ((int64_t)1 << sh) - 1) >> sh) > kOrdMaxTiles) ++sh;
+    return sh;
+}
+
 size_t slot_order_bytes(int64_t cap) {
     constexpr int B = 1 << kOrdMaxBits;
     const size_t capr = (size_t)(cap + 15) / 16 * 16;
-    return capr * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * B * sizeof(uint32_t) + (B + 2) * sizeof(int64_t) +
-           ((size_t)1 << kOrdLutBits) * sizeof(uint16_t) + 256;
+    return capr * (3 * sizeof(uint32_t)) + 2 * (size_t)kOrdMaxTiles * B * sizeof(uint32_t) +
+           (B + 2) * sizeof(int64_t) + ((size_t)1 << kOrdLutBits) * sizeof(uint16_t) + 256;
 }
 
 // Carve the order buffers out of one allocation of slot_order_bytes(cap) and
@@ -223,19 +244,21 @@ cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap) {
     constexpr int B = 1 << kOrdMaxBits;
     const size_t capr = (size_t)(cap + 15) / 16 * 16;
     c->ord_bits = ord_bits_env();
+    c->ord_tile_shift = ord_tile_shift_for(cap);
+    c->ord_ntiles = c->ord_tile_shift >= 62 ? 1 : (int)((cap + ((int64_t)1 << c->ord_tile_shift) - 1) >> c->ord_tile_shift);
     char* p = static_cast<char*>(buf);
     c->d_ord_T = reinterpret_cast<int64_t*>(p);
     p += (B + 2) * sizeof(int64_t);
-    c->d_ord_cnt = reinterpret_cast<uint32_t*>(p);
-    p += 2 * B * sizeof(uint32_t);
+    c->d_ord_cnt = reinterpret_cast<uint32_t*>(p);   // counts [tiles][B], then cursors [tiles][B]
+    p += 2 * (size_t)kOrdMaxTiles * B * sizeof(uint32_t);
     c->d_ord = reinterpret_cast<uint32_t*>(p);
     p += capr * sizeof(uint32_t);
     c->d_ord_rank = reinterpret_cast<uint32_t*>(p);
     p += capr * sizeof(uint32_t);
-    c->d_ord_key = reinterpret_cast<uint16_t*>(p);
-    p += capr * sizeof(uint16_t);
+    c->d_ord_key = reinterpret_cast<uint32_t*>(p);
+    p += capr * sizeof(uint32_t);
     c->d_ord_lut = reinterpret_cast<uint16_t*>(p);
-    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, 2 * B * sizeof(uint32_t), c->stream);
+    cudaError_t e = cudaMemsetAsync(c->d_ord_cnt, 0, 2 * (size_t)kOrdMaxTiles * B * sizeof(uint32_t), c->stream);
     if (e != cudaSuccess) return e;
     k_ord_table<<<((1 << c->ord_bits) + 1 + 255) / 256, 256, 0, c->stream>>>(
         c->d_rec, c->rec_words, c->val_words, c->N, (uint32_t)(c->hi[0] - c->lo[0]), c->ord_bits, c->d_ord_T);
@@ -246,6 +269,8 @@ cudaError_t slot_order_init(gcp_ctx* c, void* buf, int64_t cap) {
     return cudaGetLastError();
 }
 
+static uint32_t* ord_cursor(gcp_ctx* c) { return c->d_ord_cnt + (size_t)kOrdMaxTiles * (1 << kOrdMaxBits); }
+
 static OrdHistArgs make_hist_args(gcp_ctx* c, const SampleArgs& sa) {
     OrdHistArgs oh;
     oh.sa = sa;
@@ -255,6 +280,7 @@ static OrdHistArgs make_hist_args(gcp_ctx* c, const SampleArgs& sa) {
     oh.ranks = c->d_ord_rank;
     oh.totals = c->d_ord_cnt;
     oh.bits = c->ord_bits;
+    oh.tile_shift = c->ord_tile_shift;
     oh.n = sa.p + sa.q;
     return oh;
 }
@@ -268,8 +294,8 @@ static cudaError_t ord_scan(gcp_ctx* c) {
         attr = true;
     }
     const int B = 1 << c->ord_bits;
-    k_ord_scan<<<1, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(c->d_ord_cnt, c->d_ord_cnt + (1 << kOrdMaxBits),
-                                                                        B);
+    k_ord_scan<<<c->ord_ntiles, kOrdThreads, (size_t)(B + B / 32) * 4, c->stream>>>(c->d_ord_cnt, ord_cursor(c), B,
+                                                                                    c->ord_tile_shift);
     c->launches++;
     return cudaGetLastError();
 }
@@ -286,15 +312,14 @@ cudaError_t launch_slot_order(gcp_ctx* c, const SampleArgs& s, const uint32_t** 
     if (stage < 1) {
         // totals may hold an unconsumed histogram (a K2 prepared an iteration
         // that did not follow): start from zero
-        cudaError_t e = cudaMemsetAsync(totals, 0, (size_t)B * sizeof(uint32_t), c->stream);
+        cudaError_t e = cudaMemsetAsync(totals, 0, (size_t)c->ord_ntiles * B * sizeof(uint32_t), c->stream);
         if (e != cudaSuccess) return e;
         k_ord_hist<<<nb, 256, 0, c->stream>>>(make_hist_args(c, s));
         c->launches++;
     }
     cudaError_t e = ord_scan(c);
     if (e != cudaSuccess) return e;
-    k_ord_scatter<<<nb, 256, 0, c->stream>>>(c->d_ord_key, c->d_ord_rank, n, c->d_ord_cnt + (1 << kOrdMaxBits),
-                                             c->d_ord);
+    k_ord_scatter<<<nb, 256, 0, c->stream>>>(c->d_ord_key, c->d_ord_rank, n, ord_cursor(c), c->d_ord);
     c->launches++;
     return cudaGetLastError();
 }
@@ -324,7 +349,7 @@ bool ord_scatter_args(gcp_ctx* c, int64_t n, OrdScatterArgs* os, int64_t adam_ve
     if (ord_scan(c) != cudaSuccess) return false;
     os->keys = c->d_ord_key;
     os->ranks = c->d_ord_rank;
-    os->cursor = c->d_ord_cnt + (1 << kOrdMaxBits);
+    os->cursor = ord_cursor(c);
     os->order = c->d_ord;
     os->n = n;
     os->ratio = (int)std::max<int64_t>(1, adam_vecs / n);

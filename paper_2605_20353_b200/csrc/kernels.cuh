@@ -78,8 +78,8 @@ __device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16
 // bucket of slot s and its rank inside the bucket (arrival order of a global
 // atomicAdd: the scatter then needs no reservation pass)
 __device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, uint32_t it, uint64_t inv) {
-    const uint32_t b = ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
-    oh.keys[s] = (uint16_t)b;
+    const uint32_t b = ((uint32_t)(s >> oh.tile_shift) << oh.bits) | ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
+    oh.keys[s] = b;
     oh.ranks[s] = atomicAdd(oh.totals + b, 1u);
 }
 

@@ -1,0 +1,7 @@
+# round 2: compute-sanitizer --tool racecheck over every libgcp kernel on c1-sized
+# inputs (tools/sanitize_c1.py); the plain run must exit 0 first
+mkdir -p gpurun_out
+timeout 600 python tools/sanitize_c1.py > gpurun_out/r02san_plain_racecheck.log 2>&1 && echo "plain ok" && \
+timeout 2400 compute-sanitizer --tool racecheck --error-exitcode 3  \
+  python tools/sanitize_c1.py > gpurun_out/r02san_racecheck.log 2>&1
+echo "racecheck rc=$?"; tail -6 gpurun_out/r02san_racecheck.log

@@ -146,14 +146,18 @@ def test_ag_layouts_agree(gcp, orc, interleave, monkeypatch):
     assert all((c.grad_get(k) == 0).all() for k in range(3))   # G reset fused into Adam
 
 
+@pytest.mark.parametrize("tiles", ["1", "many"])
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
 @pytest.mark.parametrize("strategy", ["stratified", "semi"])
-def test_slot_order_same_gradient(gcp, orc, strategy, prec, monkeypatch):
+def test_slot_order_same_gradient(gcp, orc, strategy, prec, tiles, monkeypatch):
     """GCP_SLOT_ORDER=1: the gradient K2 visits its slots grouped by mode-1
-    position (a radix sort of the slots, kernels.cu).  Same sample set, so the
-    same gradient as the oracle's within the fp tolerance; p + q spans many
-    warps and a ragged tail."""
+    position (histogram / scan / scatter of the slots, kernels.cu; "many": the
+    slots ordered in independent tiles of 1024, the layout large p + q take).
+    Same sample set, so the same gradient as the oracle's within the fp
+    tolerance; p + q spans many warps and a ragged tail."""
     monkeypatch.setenv("GCP_SLOT_ORDER", "1")
+    if tiles == "many":
+        monkeypatch.setenv("GCP_ORD_TILE_MB", "0.001")
     dims = (20, 30, 40)
     subs, vals = _tensor("poisson")
     c = _ctx(gcp, dims, subs, vals, prec=prec)
