@@ -296,6 +296,12 @@ gcp_status gcp_layout(gcp_ctx* ctx, int* ag_interleaved, int* slot_order, int* f
 gcp_status gcp_debug_nonzero_j(gcp_ctx* ctx, uint64_t seed, uint32_t rank, uint32_t it, int64_t N,
                                int64_t first, int64_t count, int64_t* j_out);
 
+/* Test helper for reading R11's generator: for n inputs ctr_key[6i..6i+5] =
+ * (c0, c1, c2, c3, k0, k1), out[8i..8i+3] = the sampler's device
+ * Philox4x32-10 and out[8i+4..8i+7] = curand's curand_Philox4x32_10 on the
+ * same counter and key (host arrays).  Blocks. */
+gcp_status gcp_debug_philox(gcp_ctx* ctx, int64_t n, const uint32_t* ctr_key, uint32_t* out);
+
 /* Counters: it (Philox iteration word), t (Adam steps), kernel launches made
  * by this library since creation (all nullable).  Does not block. */
 gcp_status gcp_counters(gcp_ctx* ctx, uint32_t* it, int64_t* t, int64_t* launches);

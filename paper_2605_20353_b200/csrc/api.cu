@@ -1242,6 +1242,22 @@ gcp_status gcp_debug_nonzero_j(gcp_ctx* c, uint64_t seed, uint32_t rank, uint32_
     return GCP_OK;
 }
 
+gcp_status gcp_debug_philox(gcp_ctx* c, int64_t n, const uint32_t* ctr_key, uint32_t* out) {
+    ENTER(c);
+    if (n < 0 || (n > 0 && (!ctr_key || !out))) return set_error(GCP_E_ARG, "gcp_debug_philox: args");
+    if (n == 0) return GCP_OK;
+    uint32_t *d_in = nullptr, *d_out = nullptr;
+    CUDA_TRY(c, gmalloc(c, &d_in, (size_t)n * 6 * 4), "debug_philox");
+    CUDA_TRY(c, gmalloc(c, &d_out, (size_t)n * 8 * 4), "debug_philox");
+    CUDA_TRY(c, cudaMemcpyAsync(d_in, ctr_key, (size_t)n * 6 * 4, cudaMemcpyHostToDevice, c->stream), "debug_philox");
+    CUDA_TRY(c, launch_debug_philox(c, n, d_in, d_out), "debug_philox");
+    CUDA_TRY(c, cudaMemcpyAsync(out, d_out, (size_t)n * 8 * 4, cudaMemcpyDeviceToHost, c->stream), "debug_philox");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream), "debug_philox");
+    gfree(c, d_in);
+    gfree(c, d_out);
+    return GCP_OK;
+}
+
 gcp_status gcp_counters(gcp_ctx* c, uint32_t* it, int64_t* t, int64_t* launches) {
     if (!c) return set_error(GCP_E_ARG, "null context");
     if (it) *it = c->it;

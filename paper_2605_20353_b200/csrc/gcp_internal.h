@@ -286,6 +286,7 @@ cudaError_t launch_sub(gcp_ctx* c, const void* a, const void* b, void* out, int6
 cudaError_t launch_rows_in(gcp_ctx* c, const double* src, void* dst, int64_t b);    // packed rows -> layout
 cudaError_t launch_rows_out(gcp_ctx* c, const void* src, double* dst, int64_t b);   // layout -> packed rows
 int sample_kernel_blocks(gcp_ctx* c);
+cudaError_t launch_debug_philox(gcp_ctx* c, int64_t n, const uint32_t* in, uint32_t* out);
 
 // ingest.cu
 gcp_status ingest(gcp_ctx* c, const gcp_ctx* geom, int64_t nnz, const int64_t* subs, const double* vals);

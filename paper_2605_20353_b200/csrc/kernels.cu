@@ -2,6 +2,8 @@
 // helper kernels (deterministic partial-sum reduction, scale, subtract).
 #include "kernels.cuh"
 
+#include <curand_philox4x32_x.h>
+
 #include <algorithm>
 #include <string>
 
@@ -354,6 +356,26 @@ bool ord_scatter_args(gcp_ctx* c, int64_t n, OrdScatterArgs* os, int64_t adam_ve
     os->n = n;
     os->ratio = (int)std::max<int64_t>(1, adam_vecs / n);
     return true;
+}
+
+// Test helper (gcp_debug_philox): the sampler's device Philox4x32-10 and curand's
+// curand_Philox4x32_10 on the same (counter, key) inputs.
+__global__ void k_debug_philox(int64_t n, const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t* v = in + 6 * x;
+        const U64x2 w = philox(v[0], v[1], v[2], v[3], v[4], v[5]);
+        const uint4 r = curand_Philox4x32_10(make_uint4(v[0], v[1], v[2], v[3]), make_uint2(v[4], v[5]));
+        uint32_t* o = out + 8 * x;
+        o[0] = (uint32_t)w.w0; o[1] = (uint32_t)(w.w0 >> 32); o[2] = (uint32_t)w.w1; o[3] = (uint32_t)(w.w1 >> 32);
+        o[4] = r.x; o[5] = r.y; o[6] = r.z; o[7] = r.w;
+    }
+}
+
+cudaError_t launch_debug_philox(gcp_ctx* c, int64_t n, const uint32_t* in, uint32_t* out) {
+    if (n == 0) return cudaSuccess;
+    k_debug_philox<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, c->stream>>>(n, in, out);
+    c->launches++;
+    return cudaGetLastError();
 }
 
 // Fixed-order sum of n fp64 partials (deterministic; one CTA).

@@ -82,13 +82,26 @@ __global__ void __launch_bounds__(256) k_tsn_import(ncclDevComm comm, ncclWindow
     for (int k = 0; k < ta.d; ++k) {
         if (ta.nmem[k] <= 1) continue;
         const int64_t nv = ta.rows[k] * vpr;
-        for (int64_t v = tid; v < nv; v += nt) {
-            const int64_t r = v / vpr;
-            const int owner = (int)(r / ta.shard[k]);
-            if (owner == ta.me[k] || !((bm[ta.bm_off[k] + (r >> 5)] >> (r & 31)) & 1u)) continue;
-            const size_t e = (size_t)(ta.off[k] + r * ta.R_pad) + (size_t)(v % vpr) * VE;
-            const V* src = static_cast<const V*>(ncclGetLsaPointer(winA, e * sizeof(T), ta.mem[k][owner]));
-            *reinterpret_cast<V*>(A + e) = *src;
+        // four vectors per thread in flight (remote loads)
+        for (int64_t v0 = tid; v0 < nv; v0 += 4 * nt) {
+            V val[4];
+            size_t ev[4];
+            bool need[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t v = v0 + u * nt;
+                need[u] = false;
+                if (v >= nv) continue;
+                const int64_t r = v / vpr;
+                const int owner = (int)(r / ta.shard[k]);
+                if (owner == ta.me[k] || !((bm[ta.bm_off[k] + (r >> 5)] >> (r & 31)) & 1u)) continue;
+                ev[u] = (size_t)(ta.off[k] + r * ta.R_pad) + (size_t)(v % vpr) * VE;
+                val[u] = *static_cast<const V*>(ncclGetLsaPointer(winA, ev[u] * sizeof(T), ta.mem[k][owner]));
+                need[u] = true;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (need[u]) *reinterpret_cast<V*>(A + ev[u]) = val[u];
         }
     }
 }
@@ -135,43 +148,63 @@ __global__ void __launch_bounds__(256) k_tsn_export(ncclDevComm comm, ncclWindow
         // (the bits themselves are cleared by a memset after this kernel: other
         // CTAs of this launch may still be reading them here)
     }
+    // owned rows, a warp per 32-row bitmap word: lanes < g load the members'
+    // words of this iteration (one remote load each, in parallel), the warp
+    // shares them by shuffles, then walks the word's rows x vectors issuing every
+    // needed peer G load of a vector before summing (two NVLink round trips per
+    // word instead of one per member and vector)
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = tid >> 5, nwarp = nt >> 5;
     for (int k = 0; k < ta.d; ++k) {
-        const int64_t r0 = (int64_t)ta.me[k] * ta.shard[k];
-        const int64_t nv = ta.shard[k] * vpr;
+        const int64_t r0 = (int64_t)ta.me[k] * ta.shard[k], r1 = r0 + ta.shard[k];
         const int nm = ta.nmem[k];
-        for (int64_t v = tid; v < nv; v += nt) {
-            const int64_t r = r0 + v / vpr;
-            const int64_t e = ta.off[k] + r * ta.R_pad + (v % vpr) * VE;
-            const size_t ob = (size_t)e * sizeof(T);
-            V g = *static_cast<const V*>(ncclGetLocalPointer(winG, ob));
-            T* gp = reinterpret_cast<T*>(&g);
-            for (int m = 0; m < nm; ++m) {
-                if (m == ta.me[k]) continue;
-                const uint32_t* mbm = static_cast<const uint32_t*>(ncclGetLsaPointer(
-                    winBM, ((size_t)cur * ta.bm_words + ta.bm_off[k] + (r >> 5)) * sizeof(uint32_t), ta.mem[k][m]));
-                if (!((*mbm >> (r & 31)) & 1u)) continue;   // member m did not touch row r: its G row is 0
-                const V h = *static_cast<const V*>(ncclGetLsaPointer(winG, ob, ta.mem[k][m]));
-                const T* hp = reinterpret_cast<const T*>(&h);
+        const int64_t w0 = r0 >> 5, w1 = (r1 + 31) >> 5;
+        for (int64_t w = w0 + warp; w < w1; w += nwarp) {
+            uint32_t mine = 0u;
+            if (lane < nm && lane != ta.me[k] && nm > 1)
+                mine = *static_cast<const uint32_t*>(ncclGetLsaPointer(
+                    winBM, ((size_t)cur * ta.bm_words + ta.bm_off[k] + w) * sizeof(uint32_t), ta.mem[k][lane]));
+            uint32_t bits[8];
 #pragma unroll
-                for (int q = 0; q < VE; ++q) gp[q] += hp[q];
-            }
-            V a = *reinterpret_cast<const V*>(A + e);
-            V bb = *reinterpret_cast<const V*>(B + e);
-            V cc = *reinterpret_cast<const V*>(C + e);
-            T* ap = reinterpret_cast<T*>(&a);
-            T* bp = reinterpret_cast<T*>(&bb);
-            T* cp = reinterpret_cast<T*>(&cc);
+            for (int m = 0; m < 8; ++m) bits[m] = __shfl_sync(0xffffffffu, mine, m);
+            const int items = 32 * vpr;
+            for (int it = lane; it < items; it += 32) {
+                const int64_t r = (w << 5) + it / vpr;
+                if (r < r0 || r >= r1) continue;
+                const int64_t e = ta.off[k] + r * ta.R_pad + (it % vpr) * VE;
+                const size_t ob = (size_t)e * sizeof(T);
+                V g = *static_cast<const V*>(ncclGetLocalPointer(winG, ob));
+                V h[8];
 #pragma unroll
-            for (int q = 0; q < VE; ++q) {
-                const T gv = gp[q];
-                bp[q] = b1 * bp[q] + (T(1) - b1) * gv;
-                cp[q] = b2 * cp[q] + (T(1) - b2) * gv * gv;
-                const T av = ap[q] - rate * ((bp[q] * bc1) / sqrt(cp[q] * bc2 + eps));
-                ap[q] = (av < lower) ? lower : av;
+                for (int m = 0; m < 8; ++m)
+                    if (m < nm && ((bits[m] >> (r & 31)) & 1u))
+                        h[m] = *static_cast<const V*>(ncclGetLsaPointer(winG, ob, ta.mem[k][m]));
+                V a = *reinterpret_cast<const V*>(A + e);
+                V bb = *reinterpret_cast<const V*>(B + e);
+                V cc = *reinterpret_cast<const V*>(C + e);
+                T* gp = reinterpret_cast<T*>(&g);
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    if (m < nm && ((bits[m] >> (r & 31)) & 1u)) {
+                        const T* hp = reinterpret_cast<const T*>(&h[m]);
+#pragma unroll
+                        for (int q = 0; q < VE; ++q) gp[q] += hp[q];
+                    }
+                T* ap = reinterpret_cast<T*>(&a);
+                T* bp = reinterpret_cast<T*>(&bb);
+                T* cp = reinterpret_cast<T*>(&cc);
+#pragma unroll
+                for (int q = 0; q < VE; ++q) {
+                    const T gv = gp[q];
+                    bp[q] = b1 * bp[q] + (T(1) - b1) * gv;
+                    cp[q] = b2 * cp[q] + (T(1) - b2) * gv * gv;
+                    const T av = ap[q] - rate * ((bp[q] * bc1) / sqrt(cp[q] * bc2 + eps));
+                    ap[q] = (av < lower) ? lower : av;
+                }
+                *reinterpret_cast<V*>(A + e) = a;
+                *reinterpret_cast<V*>(B + e) = bb;
+                *reinterpret_cast<V*>(C + e) = cc;
             }
-            *reinterpret_cast<V*>(A + e) = a;
-            *reinterpret_cast<V*>(B + e) = bb;
-            *reinterpret_cast<V*>(C + e) = cc;
         }
     }
 }

@@ -33,7 +33,7 @@ SYMBOLS = ["gcp_create", "gcp_destroy", "gcp_last_error", "gcp_grid_plan", "gcp_
            "gcp_model_get", "gcp_sample", "gcp_sample_export", "gcp_loss_grad", "gcp_grad_get",
            "gcp_adam_step", "gcp_loss_estimate", "gcp_fit_begin", "gcp_fit_epoch", "gcp_fit",
            "gcp_counters", "gcp_profile_enable", "gcp_profile_get", "gcp_set_membership",
-           "gcp_dist_features", "gcp_layout", "gcp_debug_nonzero_j"]
+           "gcp_dist_features", "gcp_layout", "gcp_debug_nonzero_j", "gcp_debug_philox"]
 MEMBERSHIP = {"hash": 0, "sorted": 1}
 
 
@@ -92,6 +92,7 @@ def load():
         "gcp_dist_features": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "gcp_layout": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "gcp_debug_nonzero_j": [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int64, C.c_int64, C.c_int64, i64p],
+        "gcp_debug_philox": [vp, C.c_int64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)],
         "gcp_profile_enable": [vp, C.c_int],
         "gcp_profile_get": [vp, C.c_int, dp, i64p, C.c_int],
         "gcp_set_membership": [vp, C.c_int],
@@ -332,6 +333,13 @@ class Context:
         _chk(lib.gcp_debug_nonzero_j(self.h, seed, rank, it, N, first, count, _ptr(out, C.c_int64)),
              "gcp_debug_nonzero_j")
         return out
+
+    def debug_philox(self, ctr_key):
+        """(n, 6) uint32 (counter, key) -> (ours (n, 4), curand (n, 4))."""
+        a = np.ascontiguousarray(ctr_key, dtype=np.uint32).reshape(-1, 6)
+        out = np.zeros((a.shape[0], 8), np.uint32)
+        _chk(lib.gcp_debug_philox(self.h, a.shape[0], _ptr(a, C.c_uint32), _ptr(out, C.c_uint32)), "gcp_debug_philox")
+        return out[:, :4], out[:, 4:]
 
     def profile_enable(self, on=True):
         _chk(lib.gcp_profile_enable(self.h, int(on)), "gcp_profile_enable")

@@ -20,3 +20,10 @@ for s in 1e6 1e7 1e8; do
     if [ "$m" = "sync" ] && [ "$s" = "1e7" ]; then nvidia-smi nvlink -gt d > gpurun_out/r02cross4_nvlink_after.txt 2>&1; fi
   done
 done
+# c5 at 4 GPUs (LocalSGD tau=10 and sync), for the P=1 -> P=4 ratio
+for m in async sync; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29690 \
+    bench.py --gpus 4 --config c5 --mode $m --tau 10 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
+    > gpurun_out/r02cross4_c5_$m.json 2> gpurun_out/r02cross4_c5_$m.err
+  echo "c5 $m rc=$?"
+done

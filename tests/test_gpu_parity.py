@@ -544,3 +544,25 @@ def test_lean_ingest_same_tensor(gcp, orc, membership, monkeypatch):
         cx.close()
     assert np.array_equal(out[0][0][0], out[1][0][0]) and np.array_equal(out[0][0][1], out[1][0][1])
     assert np.array_equal(out[0][1], out[1][1]) and out[0][1][:20000].all()
+
+
+def test_device_philox_kat_and_curand(gcp):
+    """the sampler's device Philox4x32-10 reproduces the Random123
+    known-answer vectors (tests/golden) and equals curand's
+    curand_Philox4x32_10 on 1e5 random (counter, key) pairs."""
+    from conftest import GOLDEN
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = gcp.Context(0, None, "fp32")
+    c.tensor_create(dims, subs, vals)
+    kat = []
+    for line in (GOLDEN / "philox4x32_10_kat.txt").read_text().splitlines():
+        if line.strip() and not line.startswith("#"):
+            kat.append([int(x, 16) for x in line.split()])
+    kat = np.array(kat, dtype=np.uint64).astype(np.uint32)
+    ours, cur = c.debug_philox(kat[:, :6])
+    assert np.array_equal(ours, kat[:, 6:10]) and np.array_equal(cur, kat[:, 6:10])
+    rng = np.random.default_rng(11)
+    x = rng.integers(0, 2 ** 32, size=(100_000, 6), dtype=np.uint64).astype(np.uint32)
+    ours, cur = c.debug_philox(x)
+    assert np.array_equal(ours, cur)
