@@ -870,7 +870,7 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     // slot ids are u32: beyond 2^32 slots per rank K2 runs in slot order
     const int64_t n_slots = c->p_w + c->q_w;
     const bool order_fits = c->slot_order_forced || (double)n_slots * 4.0 <= 0.8 * (double)c->l2_bytes;
-    if (c->slot_order && !two_sided(c) && n_slots < ((int64_t)1 << 32) && order_fits) {
+    if (c->slot_order && n_slots < ((int64_t)1 << 32) && order_fits) {
         // group this iteration's slots by mode-1 position (same sample set, other
         // visiting order), so the K2 gathers / scatter-adds of one mode-1 row meet
         // in L2 (kernels.cu launch_slot_order: hand-written histogram / scan / scatter)
@@ -1209,7 +1209,7 @@ gcp_status gcp_layout(gcp_ctx* c, int* ag_interleaved, int* slot_order, int* fil
     if (ag_interleaved) *ag_interleaved = c->have_model && c->ag_interleaved ? 1 : 0;
     const bool order_fits = c->slot_order_forced || !c->bound ||
                             (double)(c->p_w + c->q_w) * 4.0 <= 0.8 * (double)c->l2_bytes;
-    if (slot_order) *slot_order = c->have_model && c->slot_order && order_fits && !two_sided(c) ? 1 : 0;
+    if (slot_order) *slot_order = c->have_model && c->slot_order && order_fits ? 1 : 0;
     if (filter) *filter = c->have_tensor && c->filter_sectors ? 1 : 0;
     return GCP_OK;
 }

@@ -25,10 +25,10 @@ def main():
     prec = "fp32" if mode == "sync32" else "fp64"
     if mode == "sync32":
         os.environ["GCP_MULTIMEM"] = "1"   # exercise the NVLS path whatever P is
-    if mode in ("sync32", "async"):
+    if mode in ("sync32", "async", "twosided"):
         # the slot-ordered K2 (on by default only when mode-1 rows spill L2, e.g.
-        # c5 blocks): standalone histogram under the fused exchange (sync32), the
-        # histogram carried by the Adam launch (async)
+        # c4 blocks): under the fused exchange (sync32), k_adam (async) and the
+        # device-driven two-sided exchange; the histogram carried by K2 each time
         os.environ["GCP_SLOT_ORDER"] = "1"
     if mode == "twosided_nccl":
         os.environ["GCP_TWOSIDED_NVL"] = "0"   # the NCCL send/recv two-sided path (twosided.cu)
