@@ -79,29 +79,32 @@ __global__ void __launch_bounds__(256) k_tsn_import(ncclDevComm comm, ncclWindow
     T* A = static_cast<T*>(ncclGetLocalPointer(winA, 0));
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     const int vpr = ta.R_pad / VE;   // 16-B vectors per row
+    // a half-warp per 32-row bitmap word (coalesced word loads; only touched
+    // rows owned elsewhere cost a remote load): each set, foreign bit's row is
+    // copied by the half-warp's lanes, all its vectors in flight at once
+    const int hl = threadIdx.x & 15;
+    const int64_t half = tid >> 4, nhalf = nt >> 4;
     for (int k = 0; k < ta.d; ++k) {
         if (ta.nmem[k] <= 1) continue;
-        const int64_t nv = ta.rows[k] * vpr;
-        // four vectors per thread in flight (remote loads)
-        for (int64_t v0 = tid; v0 < nv; v0 += 4 * nt) {
-            V val[4];
-            size_t ev[4];
-            bool need[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int64_t v = v0 + u * nt;
-                need[u] = false;
-                if (v >= nv) continue;
-                const int64_t r = v / vpr;
+        const int64_t nw = (ta.rows[k] + 31) >> 5;
+        const int64_t own0 = (int64_t)ta.me[k] * ta.shard[k], own1 = own0 + ta.shard[k];
+        for (int64_t w = half; w < nw; w += nhalf) {
+            uint32_t bits = bm[ta.bm_off[k] + w];
+            // drop my own rows
+            const int64_t rb = w << 5;
+            for (int i = 0; i < 32 && bits; ++i)
+                if (rb + i >= own0 && rb + i < own1) bits &= ~(1u << i);
+            while (bits) {
+                const int i = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int64_t r = rb + i;
                 const int owner = (int)(r / ta.shard[k]);
-                if (owner == ta.me[k] || !((bm[ta.bm_off[k] + (r >> 5)] >> (r & 31)) & 1u)) continue;
-                ev[u] = (size_t)(ta.off[k] + r * ta.R_pad) + (size_t)(v % vpr) * VE;
-                val[u] = *static_cast<const V*>(ncclGetLsaPointer(winA, ev[u] * sizeof(T), ta.mem[k][owner]));
-                need[u] = true;
+                for (int v = hl; v < vpr; v += 16) {
+                    const size_t e = (size_t)(ta.off[k] + r * ta.R_pad) + (size_t)v * VE;
+                    *reinterpret_cast<V*>(A + e) =
+                        *static_cast<const V*>(ncclGetLsaPointer(winA, e * sizeof(T), ta.mem[k][owner]));
+                }
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (need[u]) *reinterpret_cast<V*>(A + ev[u]) = val[u];
         }
     }
 }
@@ -137,12 +140,23 @@ __global__ void __launch_bounds__(256) k_tsn_export(ncclDevComm comm, ncclWindow
 #pragma unroll
         for (int q = 0; q < VE; ++q) zp[q] = T(0);
         for (int k = 0; k < ta.d; ++k) {
-            const int64_t nv = ta.rows[k] * vpr;
-            for (int64_t v = tid; v < nv; v += nt) {
-                const int64_t r = v / vpr;
-                // modes without a slice group keep no bits: their G rows are cleared whole
-                if (ta.nmem[k] > 1 && !((pbm[ta.bm_off[k] + (r >> 5)] >> (r & 31)) & 1u)) continue;
-                *reinterpret_cast<V*>(Gp + ta.off[k] + r * ta.R_pad + (v % vpr) * VE) = z;
+            if (ta.nmem[k] <= 1) {   // no slice group, no bits: the mode's G rows are cleared whole
+                const int64_t nv = ta.rows[k] * vpr;
+                for (int64_t v = tid; v < nv; v += nt) *reinterpret_cast<V*>(Gp + ta.off[k] + v * VE) = z;
+                continue;
+            }
+            // a half-warp per bitmap word: the previous iteration's touched rows only
+            const int hl = threadIdx.x & 15;
+            const int64_t nw = (ta.rows[k] + 31) >> 5;
+            for (int64_t w = tid >> 4; w < nw; w += nt >> 4) {
+                uint32_t bits = pbm[ta.bm_off[k] + w];
+                while (bits) {
+                    const int i = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int64_t r = (w << 5) + i;
+                    for (int v = hl; v < vpr; v += 16)
+                        *reinterpret_cast<V*>(Gp + ta.off[k] + r * ta.R_pad + v * VE) = z;
+                }
             }
         }
         // (the bits themselves are cleared by a memset after this kernel: other
