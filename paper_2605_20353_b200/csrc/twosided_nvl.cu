@@ -12,13 +12,13 @@
 //                           Adam); every touched row owned elsewhere is loaded
 //                           from its owner's A window into the local copy
 //   K2                      unchanged: fused sampling-MTTKRP into the local G
-//   export  (k_tsn_export)  LSA barrier (every rank's K2 done); the owner of a
-//                           row sums its own G row and the G rows of exactly
+//   export  (k_tsn_pull)    LSA barrier (every rank's K2 done); the owner of a
+//                           row adds to its own G row the G rows of exactly
 //                           the members whose bitmap marks the row (the
 //                           paper's export of partial rows to their owner,
-//                           pulled by the owner), runs Alg. 1 on its rows, and
-//                           zeroes the previous parity's G rows (a memset after
-//                           it clears the previous parity's bits)
+//                           pulled by the owner) and zeroes the previous
+//                           parity's G rows; then k_adam (Alg. 1) on the owned
+//                           rows and a memset of the previous parity's bits
 //
 // The per-iteration request lists, counts exchange, host synchronisation and
 // grouped send/recv of the NCCL two-sided path (twosided.cu) disappear: only
@@ -67,9 +67,11 @@ template <typename T> struct TVec;
 template <> struct TVec<float> { using type = float4; static constexpr int n = 4; };
 template <> struct TVec<double> { using type = double2; static constexpr int n = 2; };
 
-// every touched row owned by another member: its owner's A row into the local copy
+// every touched row owned by another member: its owner's A row into the local
+// copy.  A thread per 16-B vector of the non-owned rows, four in flight (the
+// bitmap words are L1 hits shared by the warp; only touched rows cost a remote load).
 template <typename T>
-__global__ void __launch_bounds__(256) k_tsn_import(ncclDevComm comm, ncclWindow_t winA, ncclWindow_t winBM,
+__global__ void __launch_bounds__(512) k_tsn_import(ncclDevComm comm, ncclWindow_t winA, ncclWindow_t winBM,
                                                     int cur, const TsnArgs ta) {
     using V = typename TVec<T>::type;
     constexpr int VE = TVec<T>::n;
@@ -79,145 +81,120 @@ __global__ void __launch_bounds__(256) k_tsn_import(ncclDevComm comm, ncclWindow
     T* A = static_cast<T*>(ncclGetLocalPointer(winA, 0));
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     const int vpr = ta.R_pad / VE;   // 16-B vectors per row
-    // a half-warp per 32-row bitmap word (coalesced word loads; only touched
-    // rows owned elsewhere cost a remote load): each set, foreign bit's row is
-    // copied by the half-warp's lanes, all its vectors in flight at once
-    const int hl = threadIdx.x & 15;
-    const int64_t half = tid >> 4, nhalf = nt >> 4;
     for (int k = 0; k < ta.d; ++k) {
         if (ta.nmem[k] <= 1) continue;
-        const int64_t nw = (ta.rows[k] + 31) >> 5;
-        const int64_t own0 = (int64_t)ta.me[k] * ta.shard[k], own1 = own0 + ta.shard[k];
-        for (int64_t w = half; w < nw; w += nhalf) {
-            uint32_t bits = bm[ta.bm_off[k] + w];
-            // drop my own rows
-            const int64_t rb = w << 5;
-            for (int i = 0; i < 32 && bits; ++i)
-                if (rb + i >= own0 && rb + i < own1) bits &= ~(1u << i);
-            while (bits) {
-                const int i = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int64_t r = rb + i;
-                const int owner = (int)(r / ta.shard[k]);
-                for (int v = hl; v < vpr; v += 16) {
-                    const size_t e = (size_t)(ta.off[k] + r * ta.R_pad) + (size_t)v * VE;
-                    *reinterpret_cast<V*>(A + e) =
-                        *static_cast<const V*>(ncclGetLsaPointer(winA, e * sizeof(T), ta.mem[k][owner]));
-                }
+        const int64_t own0 = (int64_t)ta.me[k] * ta.shard[k];
+        const int64_t nv = (ta.rows[k] - ta.shard[k]) * vpr;   // vectors of the rows owned elsewhere
+        for (int64_t v0 = tid; v0 < nv; v0 += 4 * nt) {
+            V val[4];
+            int64_t ev[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t v = v0 + u * nt;
+                ev[u] = -1;
+                if (v >= nv) continue;
+                int64_t r = v / vpr;
+                if (r >= own0) r += ta.shard[k];   // skip my own shard
+                if (!((bm[ta.bm_off[k] + (r >> 5)] >> (r & 31)) & 1u)) continue;
+                ev[u] = ta.off[k] + r * ta.R_pad + (v % vpr) * VE;
+                val[u] = *static_cast<const V*>(
+                    ncclGetLsaPointer(winA, (size_t)ev[u] * sizeof(T), ta.mem[k][(int)(r / ta.shard[k])]));
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ev[u] >= 0) *reinterpret_cast<V*>(A + ev[u]) = val[u];
         }
     }
 }
 
-// owned rows: G summed over the members that touched them, Alg. 1, then the
-// previous parity's G rows and bits cleared
+// The owner's side of the export: after the barrier (every member's K2 of this
+// iteration is complete) each owned row's G gets the G rows of exactly the
+// members whose bitmap marks it (a thread per 16-B vector, the members' bit
+// words and rows for four vectors in flight), and the previous parity's G rows
+// are cleared (a thread per bit word).  Adam on the owned rows follows as the
+// ordinary k_adam launch (tsn_export).
 template <typename T>
-__global__ void __launch_bounds__(256) k_tsn_export(ncclDevComm comm, ncclWindow_t winA, ncclWindow_t winG,
-                                                    ncclWindow_t winGprev, ncclWindow_t winBM, int cur,
-                                                    T* __restrict__ B, T* __restrict__ C, const TsnArgs ta, T rate,
-                                                    T b1, T b2, T eps, T bc1, T bc2, T lower, const DevStep* step,
-                                                    long long t_off) {
+__global__ void __launch_bounds__(512) k_tsn_pull(ncclDevComm comm, ncclWindow_t winG, ncclWindow_t winGprev,
+                                                  ncclWindow_t winBM, int cur, const TsnArgs ta) {
     using V = typename TVec<T>::type;
     constexpr int VE = TVec<T>::n;
-    if (step) {   // graph replay: t = t0 + offset, bias corrections in fp64 from it
-        const double t = (double)(step->t + t_off);
-        rate = (T)step->rate;
-        bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
-        bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
-    }
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamLsa(comm), comm.lsaBarrier, blockIdx.x);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // every member's K2 of this iteration is complete
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     const int vpr = ta.R_pad / VE;
-    T* A = static_cast<T*>(ncclGetLocalPointer(winA, 0));
-    // clear the previous parity: my G rows marked by my previous bits, then the bits
+    V z;
+    T* zp = reinterpret_cast<T*>(&z);
+#pragma unroll
+    for (int q = 0; q < VE; ++q) zp[q] = T(0);
+    // clear the previous parity: my G rows marked by my previous bits (modes
+    // without a slice group keep no bits: cleared whole).  The bits themselves
+    // are cleared by a memset after this kernel (other CTAs may still read them).
     {
         const uint32_t* pbm =
             static_cast<const uint32_t*>(ncclGetLocalPointer(winBM, 0)) + (int64_t)(cur ^ 1) * ta.bm_words;
         T* Gp = static_cast<T*>(ncclGetLocalPointer(winGprev, 0));
-        V z;
-        T* zp = reinterpret_cast<T*>(&z);
-#pragma unroll
-        for (int q = 0; q < VE; ++q) zp[q] = T(0);
         for (int k = 0; k < ta.d; ++k) {
-            if (ta.nmem[k] <= 1) {   // no slice group, no bits: the mode's G rows are cleared whole
+            if (ta.nmem[k] <= 1) {
                 const int64_t nv = ta.rows[k] * vpr;
                 for (int64_t v = tid; v < nv; v += nt) *reinterpret_cast<V*>(Gp + ta.off[k] + v * VE) = z;
                 continue;
             }
-            // a half-warp per bitmap word: the previous iteration's touched rows only
-            const int hl = threadIdx.x & 15;
             const int64_t nw = (ta.rows[k] + 31) >> 5;
-            for (int64_t w = tid >> 4; w < nw; w += nt >> 4) {
+            for (int64_t w = tid; w < nw; w += nt) {
                 uint32_t bits = pbm[ta.bm_off[k] + w];
                 while (bits) {
                     const int i = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    const int64_t r = (w << 5) + i;
-                    for (int v = hl; v < vpr; v += 16)
-                        *reinterpret_cast<V*>(Gp + ta.off[k] + r * ta.R_pad + v * VE) = z;
+                    T* row = Gp + ta.off[k] + ((w << 5) + i) * ta.R_pad;
+                    for (int v = 0; v < vpr; ++v) *reinterpret_cast<V*>(row + v * VE) = z;
                 }
             }
         }
-        // (the bits themselves are cleared by a memset after this kernel: other
-        // CTAs of this launch may still be reading them here)
     }
-    // owned rows, a warp per 32-row bitmap word: lanes < g load the members'
-    // words of this iteration (one remote load each, in parallel), the warp
-    // shares them by shuffles, then walks the word's rows x vectors issuing every
-    // needed peer G load of a vector before summing (two NVLink round trips per
-    // word instead of one per member and vector)
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = tid >> 5, nwarp = nt >> 5;
+    T* G = static_cast<T*>(ncclGetLocalPointer(winG, 0));
     for (int k = 0; k < ta.d; ++k) {
-        const int64_t r0 = (int64_t)ta.me[k] * ta.shard[k], r1 = r0 + ta.shard[k];
         const int nm = ta.nmem[k];
-        const int64_t w0 = r0 >> 5, w1 = (r1 + 31) >> 5;
-        for (int64_t w = w0 + warp; w < w1; w += nwarp) {
-            uint32_t mine = 0u;
-            if (lane < nm && lane != ta.me[k] && nm > 1)
-                mine = *static_cast<const uint32_t*>(ncclGetLsaPointer(
-                    winBM, ((size_t)cur * ta.bm_words + ta.bm_off[k] + w) * sizeof(uint32_t), ta.mem[k][lane]));
-            uint32_t bits[8];
+        if (nm <= 1) continue;
+        const int64_t r0 = (int64_t)ta.me[k] * ta.shard[k];
+        const int64_t nv = ta.shard[k] * vpr;
+        for (int64_t v0 = tid; v0 < nv; v0 += 4 * nt) {
+            uint32_t bits[4][8];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) bits[m] = __shfl_sync(0xffffffffu, mine, m);
-            const int items = 32 * vpr;
-            for (int it = lane; it < items; it += 32) {
-                const int64_t r = (w << 5) + it / vpr;
-                if (r < r0 || r >= r1) continue;
-                const int64_t e = ta.off[k] + r * ta.R_pad + (it % vpr) * VE;
-                const size_t ob = (size_t)e * sizeof(T);
-                V g = *static_cast<const V*>(ncclGetLocalPointer(winG, ob));
-                V h[8];
+            for (int u = 0; u < 4; ++u) {
+                const int64_t v = v0 + u * nt;
+                const int64_t r = r0 + (v < nv ? v / vpr : 0);
+                const size_t wb = ((size_t)cur * ta.bm_words + ta.bm_off[k] + (r >> 5)) * sizeof(uint32_t);
 #pragma unroll
                 for (int m = 0; m < 8; ++m)
-                    if (m < nm && ((bits[m] >> (r & 31)) & 1u))
-                        h[m] = *static_cast<const V*>(ncclGetLsaPointer(winG, ob, ta.mem[k][m]));
-                V a = *reinterpret_cast<const V*>(A + e);
-                V bb = *reinterpret_cast<const V*>(B + e);
-                V cc = *reinterpret_cast<const V*>(C + e);
+                    bits[u][m] = (v < nv && m < nm && m != ta.me[k])
+                                     ? *static_cast<const uint32_t*>(ncclGetLsaPointer(winBM, wb, ta.mem[k][m]))
+                                     : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t v = v0 + u * nt;
+                if (v >= nv) continue;
+                const int64_t r = r0 + v / vpr;
+                const int64_t e = ta.off[k] + r * ta.R_pad + (v % vpr) * VE;
+                V h[8];
+                bool any = false;
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    if ((bits[u][m] >> (r & 31)) & 1u) {
+                        h[m] = *static_cast<const V*>(ncclGetLsaPointer(winG, (size_t)e * sizeof(T), ta.mem[k][m]));
+                        any = true;
+                    }
+                if (!any) continue;
+                V g = *reinterpret_cast<const V*>(G + e);
                 T* gp = reinterpret_cast<T*>(&g);
 #pragma unroll
                 for (int m = 0; m < 8; ++m)
-                    if (m < nm && ((bits[m] >> (r & 31)) & 1u)) {
+                    if ((bits[u][m] >> (r & 31)) & 1u) {
                         const T* hp = reinterpret_cast<const T*>(&h[m]);
 #pragma unroll
                         for (int q = 0; q < VE; ++q) gp[q] += hp[q];
                     }
-                T* ap = reinterpret_cast<T*>(&a);
-                T* bp = reinterpret_cast<T*>(&bb);
-                T* cp = reinterpret_cast<T*>(&cc);
-#pragma unroll
-                for (int q = 0; q < VE; ++q) {
-                    const T gv = gp[q];
-                    bp[q] = b1 * bp[q] + (T(1) - b1) * gv;
-                    cp[q] = b2 * cp[q] + (T(1) - b2) * gv * gv;
-                    const T av = ap[q] - rate * ((bp[q] * bc1) / sqrt(cp[q] * bc2 + eps));
-                    ap[q] = (av < lower) ? lower : av;
-                }
-                *reinterpret_cast<V*>(A + e) = a;
-                *reinterpret_cast<V*>(B + e) = bb;
-                *reinterpret_cast<V*>(C + e) = cc;
+                *reinterpret_cast<V*>(G + e) = g;
             }
         }
     }
@@ -292,33 +269,42 @@ gcp_status tsn_import(gcp_ctx* c, const SampleArgs& sa) {
     return GCP_OK;
 }
 
-// export + Adam on the owned rows (gcp_adam_step)
+// export + Adam on the owned rows (gcp_adam_step): the pull kernel, Alg. 1 on
+// the owned shards of the current G (k_adam; G is cleared a parity later), the
+// previous parity's bits cleared
 gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower) {
     const TsnArgs ta = tsn_args(c);
     const int cur = (int)(c->it & 1);
-    const double bc1 = 1.0 / (1.0 - pow(p->beta1, (double)c->t));
-    const double bc2 = 1.0 / (1.0 - pow(p->beta2, (double)c->t));
-    const DevStep* step = c->capturing ? c->d_step : nullptr;
-    const long long toff = (long long)(c->t - c->graph_t0);
     cudaEvent_t ev;
     prof_begin(c, PROF_COMM, &ev);
     if (c->prec == GCP_FP32)
-        k_tsn_export<float><<<c->fused_ctas, 256, 0, c->stream>>>(
-            c->devcomm, c->winA, c->winG[cur], c->winG[cur ^ 1], c->winBM, cur, (float*)c->d_B, (float*)c->d_C, ta,
-            (float)p->rate, (float)p->beta1, (float)p->beta2, (float)p->eps, (float)bc1, (float)bc2, (float)lower,
-            step, toff);
+        k_tsn_pull<float><<<c->fused_ctas, 512, 0, c->stream>>>(c->devcomm, c->winG[cur], c->winG[cur ^ 1], c->winBM,
+                                                                cur, ta);
     else
-        k_tsn_export<double><<<c->fused_ctas, 256, 0, c->stream>>>(
-            c->devcomm, c->winA, c->winG[cur], c->winG[cur ^ 1], c->winBM, cur, (double*)c->d_B, (double*)c->d_C, ta,
-            p->rate, p->beta1, p->beta2, p->eps, bc1, bc2, lower, step, toff);
+        k_tsn_pull<double><<<c->fused_ctas, 512, 0, c->stream>>>(c->devcomm, c->winG[cur], c->winG[cur ^ 1],
+                                                                 c->winBM, cur, ta);
     TSN_CUDA(c, cudaGetLastError(), "two-sided export");
+    c->launches += 1;
+    prof_end(c, PROF_COMM, ev);
+    Segment seg;
+    seg.n = 0;
+    for (int k = 0; k < c->d; ++k) {
+        seg.start[seg.n] = c->off[k] + (int64_t)c->slice_rank[k] * (c->rows[k] / c->slice_size[k]) * c->R_pad;
+        seg.len[seg.n] = (c->rows[k] / c->slice_size[k]) * c->R_pad;
+        seg.n++;
+    }
+    prof_begin(c, PROF_ADAM, &ev);
+    TSN_CUDA(c, launch_adam(c, seg, c->d_A, cur ? c->d_G2 : c->d_G, c->d_B, c->d_C, p->rate, p->beta1, p->beta2,
+                            p->eps, lower, c->capturing ? c->t - c->graph_t0 : c->t, 0, c->R_pad,
+                            c->capturing ? c->d_step : nullptr),
+             "two-sided adam");
+    c->launches += 1;
+    prof_end(c, PROF_ADAM, ev);
     // the previous parity's bits: every member read them in the previous export
     // (all passed this export's barrier), the next touch pass writes them
     TSN_CUDA(c, cudaMemsetAsync(static_cast<uint32_t*>(c->d_bm) + (int64_t)(cur ^ 1) * ta.bm_words, 0,
                                 (size_t)ta.bm_words * sizeof(uint32_t), c->stream),
              "two-sided bits");
-    c->launches += 1;
-    prof_end(c, PROF_COMM, ev);
     return GCP_OK;
 }
 
