@@ -160,6 +160,7 @@ __device__ __forceinline__ void zero_candidate(const SampleArgs& a, uint32_t zs,
     for (int g = 0; g < (D + 1) / 2; ++g) {
         const U64x2 w = philox(zs, a.rank, (a.kind_z << 28) | (att << 4) | (uint32_t)g, iter_word(a), k0, k1);
         c[2 * g] = (uint32_t)range_map(w.w0, a.bdim[2 * g]);
+        GCP_CHECK(c[2 * g] < a.bdim[2 * g], "zero candidate coordinate", c[2 * g], a.bdim[2 * g]);
         if (2 * g + 1 < D) c[2 * g + 1] = (uint32_t)range_map(w.w1, a.bdim[2 * g + 1]);
     }
 }
@@ -195,6 +196,7 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
         // nonzero slot: j uniform over [0, N) with replacement
         const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, iter_word(a), k0, k1);
         const uint64_t j = range_map(w.w0, (uint64_t)a.N);
+        GCP_CHECK(j < (uint64_t)a.N || a.rec_words == 0, "record index >= N", j, a.N);
         const uint4* r = reinterpret_cast<const uint4*>(a.rec + j * a.rec_words);
         P.w0 = __ldg(r);
         if (VW + D > 4) P.w1 = __ldg(r + 1);
@@ -223,6 +225,7 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
         P.state = 4;
         return P;
     }
+    GCP_CHECK(b + 4 <= (a.hash_mask + 1) * (a.key128 ? 2 : 1), "hash bucket past the table", b, a.hash_mask);
     const uint4* h = reinterpret_cast<const uint4*>(a.hash + b);
     P.w0 = __ldg(h);
     P.w1 = __ldg(h + 1);

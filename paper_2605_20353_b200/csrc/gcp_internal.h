@@ -12,6 +12,22 @@
 
 #include "../../include/gcp.h"
 
+// Bounds-checked build (python paper_2605_20353_b200/build.py --variant bounds
+// -DGCP_BOUNDS_CHECK; loaded with GCP_LIB=libgcp_bounds.so): device indices of
+// the hot path are checked and the first violations printed as "GCP-BOUNDS".
+// compute-sanitizer is closed on this GPU pool, so this is the memory-safety
+// check (tools/sanitize_c1.py, profiles/r02_bounds.sh).
+#ifdef GCP_BOUNDS_CHECK
+#define GCP_CHECK(cond, what, x, y)                                                                  \
+    do {                                                                                           \
+        if (!(cond)) printf("GCP-BOUNDS %s: %lld %lld\n", what, (long long)(x), (long long)(y));   \
+    } while (0)
+#else
+#define GCP_CHECK(cond, what, x, y) \
+    do {                            \
+    } while (0)
+#endif
+
 namespace gcp {
 
 constexpr int kMaxModes = 8;          // array capacity

@@ -205,8 +205,11 @@ __global__ void __launch_bounds__(256) k_ord_scatter(const uint32_t* __restrict_
                                                     const uint32_t* __restrict__ ranks, int64_t n,
                                                     const uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += nt)
-        order[__ldg(cursor + keys[s]) + ranks[s]] = (uint32_t)s;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += nt) {
+        const uint32_t pos = __ldg(cursor + keys[s]) + ranks[s];
+        GCP_CHECK(pos < (uint64_t)n, "order position >= p + q", pos, n);
+        order[pos] = (uint32_t)s;
+    }
 }
 
 static int64_t lut_cells(int64_t N, int* shift) {

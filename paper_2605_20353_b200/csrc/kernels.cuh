@@ -66,6 +66,7 @@ __device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16
     if (s < a.p) {
         const U64x2 w = philox((uint32_t)s, a.rank, a.kind_nz << 28, it, k0, k1);
         const uint64_t j = range_map(w.w0, (uint64_t)a.N);
+        GCP_CHECK(j < (uint64_t)a.N, "nonzero index for the bucket lookup", j, a.N);
         return __ldg(lut + (j >> lut_shift));
     }
     const U64x2 w = philox((uint32_t)(s - a.p), a.rank, a.kind_z << 28, it, k0, k1);
@@ -79,6 +80,7 @@ __device__ __forceinline__ uint32_t ord_bucket(const SampleArgs& a, const uint16
 // atomicAdd: the scatter then needs no reservation pass)
 __device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, uint32_t it, uint64_t inv) {
     const uint32_t b = ((uint32_t)(s >> oh.tile_shift) << oh.bits) | ord_bucket(oh.sa, oh.lut, oh.lut_shift, oh.bits, s, it, inv);
+    GCP_CHECK((b & ((1u << oh.bits) - 1)) < (1u << oh.bits) && s < oh.n, "histogram slot", s, b);
     oh.keys[s] = b;
     oh.ranks[s] = atomicAdd(oh.totals + b, 1u);
 }
@@ -100,7 +102,10 @@ template <int D, int NV> struct SampleGeom {
 
 // position s of the visiting order -> slot (identity unless a slot order is given)
 __device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t s, int64_t total) {
-    return (a.order && s < total) ? (int64_t)__ldg(a.order + s) : s;
+    if (!(a.order && s < total)) return s;
+    const int64_t v = (int64_t)__ldg(a.order + s);
+    GCP_CHECK(v < total, "order entry >= p + q", v, total);
+    return v;
 }
 
 template <typename T, int D, int GL, int NV>
@@ -178,6 +183,7 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                 rf[b] = __shfl_sync(0xffffffffu, flags, src);
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
+                    GCP_CHECK(!(rf[b] & 1) || rc[b][k] < sa.bdim[k], "gather row", rc[b][k], sa.bdim[k]);
                     const T* row = A + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
@@ -213,6 +219,7 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                 if (!kp.loss_mode && ok) {
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
+                        GCP_CHECK(rc[b][k] < sa.bdim[k], "scatter row", rc[b][k], sa.bdim[k]);
                         T* grow = G + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {

@@ -59,7 +59,10 @@ __global__ void k_tsn_touch(const SampleArgs sa, uint32_t* __restrict__ bm, TsnA
         const Sample<T, D> smp = draw_sample<T, D>(sa, s);
 #pragma unroll
         for (int k = 0; k < D; ++k)
-            if (ta.nmem[k] > 1) atomicOr(bm + ta.bm_off[k] + (smp.c[k] >> 5), 1u << (smp.c[k] & 31));
+            if (ta.nmem[k] > 1) {
+                GCP_CHECK(smp.c[k] < ta.rows[k], "touched row", smp.c[k], ta.rows[k]);
+                atomicOr(bm + ta.bm_off[k] + (smp.c[k] >> 5), 1u << (smp.c[k] & 31));
+            }
     }
 }
 
@@ -95,6 +98,7 @@ __global__ void __launch_bounds__(512) k_tsn_import(ncclDevComm comm, ncclWindow
                 if (v >= nv) continue;
                 int64_t r = v / vpr;
                 if (r >= own0) r += ta.shard[k];   // skip my own shard
+                GCP_CHECK(r < ta.rows[k] && r / ta.shard[k] < ta.nmem[k], "import row", r, ta.rows[k]);
                 if (!((bm[ta.bm_off[k] + (r >> 5)] >> (r & 31)) & 1u)) continue;
                 ev[u] = ta.off[k] + r * ta.R_pad + (v % vpr) * VE;
                 val[u] = *static_cast<const V*>(
