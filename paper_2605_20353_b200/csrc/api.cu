@@ -132,6 +132,9 @@ void free_model(gcp_ctx* c) {
     fused_free(c);                             // symmetric A / G windows (collective)
     if (c->ag_interleaved) c->d_G = nullptr;   // a view into d_A
     c->ag_interleaved = false;
+    gfree(c, c->d_peer_bases);
+    c->d_peer_bases = nullptr;
+    c->tsn_peer = false;
     void** bufs[] = {&c->d_A, &c->d_G, &c->d_B, &c->d_C, &c->d_lambda, &c->d_Ack, &c->d_Bck, &c->d_Cck,
                      &c->d_U,  &c->d_Bs, &c->d_Cs};
     for (void** b : bufs) {
@@ -201,6 +204,22 @@ ModelArgs model_args(const gcp_ctx* c) {
     for (int k = 0; k < kMaxModes; ++k) m.off[k] = k < c->d ? c->off[k] * mult : 0;
     m.R_pad = c->R_pad;
     m.row_stride = c->ag_stride;
+    m.peerA = nullptr;
+    m.peerG = nullptr;
+    for (int k = 0; k < kMaxModes; ++k) {
+        m.shard[k] = 1;
+        m.nmem[k] = 1;
+        for (int j = 0; j < 8; ++j) m.mem[k][j] = 0;
+    }
+    if (c->tsn_peer) {
+        m.peerA = const_cast<const void* const*>(c->d_peer_bases);
+        m.peerG = c->d_peer_bases + ((c->it & 1) ? 16 : 8);
+        for (int k = 0; k < c->d; ++k) {
+            m.shard[k] = c->rows[k] / c->slice_size[k];
+            m.nmem[k] = c->fnmem[k];
+            for (int j = 0; j < c->fnmem[k]; ++j) m.mem[k][j] = c->fmem[k][j];
+        }
+    }
     return m;
 }
 
@@ -664,7 +683,11 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     // export (twosided_nvl.cu); both keep A, G, G2 in symmetric NVLink windows
     const bool use_fused = fused_possible(c) || tsn_possible(c);
     if (use_fused) ST_TRY(fused_alloc(c, bytes));
-    if (use_fused && two_sided(c)) ST_TRY(tsn_alloc_bitmap(c));
+    c->tsn_peer = false;
+    if (use_fused && two_sided(c)) {
+        if (tsn_peer_wanted()) ST_TRY(tsn_peer_setup(c));   // K2 reaches the owners' rows directly
+        else ST_TRY(tsn_alloc_bitmap(c));
+    }
     {
         void** bufs[] = {&c->d_A, &c->d_B, &c->d_C};
         for (void** b : bufs) {
@@ -862,7 +885,7 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     const int stratified = c->strategy == GCP_STRATIFIED;
     const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
     // two-sided layout (row f3): touch pass + import of the rows owned elsewhere
-    if (two_sided(c) && !c->have_grad) ST_TRY(c->fused ? tsn_import(c, s) : twosided_import(c, s));
+    if (two_sided(c) && !c->have_grad && !c->tsn_peer) ST_TRY(c->fused ? tsn_import(c, s) : twosided_import(c, s));
     const ModelArgs m = model_args(c);
     const int with_loss = sampled_loss_out != nullptr;
     cudaEvent_t ev;
@@ -942,7 +965,8 @@ gcp_status gcp_adam_step(gcp_ctx* c, const gcp_adam_params* p) {
     c->t += 1;
     if (c->fused) {   // sync P > 1: reduce-scatter + Adam + all-gather in one NVLink kernel;
                       // two-sided: export of the touched rows + Adam on the owned rows
-        ST_TRY(two_sided(c) ? tsn_export(c, p, lower) : fused_exchange(c, p, lower));
+        ST_TRY(!two_sided(c) ? fused_exchange(c, p, lower) : c->tsn_peer ? tsn_peer_step(c, p, lower)
+                                                                         : tsn_export(c, p, lower));
         c->it += 1;
         c->have_grad = false;
         return GCP_OK;
@@ -1016,7 +1040,8 @@ gcp_status gcp_loss_estimate(gcp_ctx* c, gcp_loss loss, int64_t f_nz, int64_t f_
     int64_t p, q;
     local_counts(c, f_nz, f_z, &p, &q);
     double* dout = (double*)c->d_partials + c->partials_cap;
-    if (two_sided(c)) ST_TRY(dist_sync_exchange_post(c));   // f-samples read any block row: refresh them
+    // f-samples read any block row: refresh them (peer access reads the owners' rows)
+    if (two_sided(c) && !c->tsn_peer) ST_TRY(dist_sync_exchange_post(c));
     ST_TRY(run_loss_kernel(c, loss, p, q, seed, 0xFFFFFFFFu, KIND_F_NZ, KIND_F_Z, 1, 0, PROF_LOSS, 1, dout));
     if (c->P > 1) ST_TRY(dist_allreduce_scalar(c, dout));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_scalar, dout, 8, cudaMemcpyDeviceToHost, c->stream), "loss_estimate");

@@ -90,6 +90,15 @@ struct ModelArgs {
     int64_t off[kMaxModes];   // element offset of mode k's first row in the A (and G) buffer
     int R_pad;
     int row_stride;           // elements between consecutive rows (R_pad, or 2 R_pad when A/G interleave)
+    // two-sided over NVLink, peer access (twosided_nvl.cu): rows of mode k are
+    // owned by slice member r / shard[k] (LSA rank mem[k][.]); K2 gathers them
+    // from the owner's A window and scatter-adds into the owner's G window.
+    // peerA == null: every row is local.
+    const void* const* peerA; // [LSA ranks] window bases of A
+    void* const* peerG;       // [LSA ranks] window bases of the current G parity
+    int64_t shard[kMaxModes];
+    int nmem[kMaxModes];
+    int mem[kMaxModes][8];
 };
 
 // The slot-order histogram pass of the NEXT iteration, carried by the gradient
@@ -158,6 +167,8 @@ struct gcp_ctx {
     void* d_G2 = nullptr;                         // second G buffer (iteration parity)
     void* d_bm = nullptr;                         // two-sided over NVLink: touched-row bits (2 parities)
     ncclWindow_t winBM = nullptr;
+    bool tsn_peer = false;                        // two-sided over NVLink by peer access (no import / export)
+    void** d_peer_bases = nullptr;                // [3][8]: LSA bases of A, G, G2 of every rank
     // windows of the previous model kept registered for the next one of the same
     // size (a replace-ingest job skips the collective deregister / register)
     void* fcache_buf[3] = {nullptr, nullptr, nullptr};
@@ -335,6 +346,9 @@ bool tsn_possible(gcp_ctx* c);
 size_t tsn_bitmap_bytes(const gcp_ctx* c);
 gcp_status tsn_import(gcp_ctx* c, const SampleArgs& sa);
 gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower);
+gcp_status tsn_peer_setup(gcp_ctx* c);                          // the LSA base table (after fused_alloc)
+gcp_status tsn_peer_step(gcp_ctx* c, const gcp_adam_params* p, double lower);   // barrier + Adam + barrier
+bool tsn_peer_wanted();                                         // GCP_TWOSIDED_NVL=peer
 
 }  // namespace gcp
 

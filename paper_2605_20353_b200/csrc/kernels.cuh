@@ -184,7 +184,10 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
                     GCP_CHECK(!(rf[b] & 1) || rc[b][k] < sa.bdim[k], "gather row", rc[b][k], sa.bdim[k]);
-                    const T* row = A + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
+                    const T* Ak = A;
+                    if (ma.peerA && ma.nmem[k] > 1)   // the owner's A window (peer access over NVLink)
+                        Ak = static_cast<const T*>(ma.peerA[ma.mem[k][(int)(rc[b][k] / (uint64_t)ma.shard[k])]]);
+                    const T* row = Ak + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
                         if ((rf[b] & 1) && vok[v]) ldg_vec<T, VE>(a[b][k][v], row + (gl + v * GL) * VE);
@@ -220,7 +223,10 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
                         GCP_CHECK(rc[b][k] < sa.bdim[k], "scatter row", rc[b][k], sa.bdim[k]);
-                        T* grow = G + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
+                        T* Gk = G;
+                        if (ma.peerA && ma.nmem[k] > 1)   // the owner's G window: red.add over NVLink
+                            Gk = static_cast<T*>(ma.peerG[ma.mem[k][(int)(rc[b][k] / (uint64_t)ma.shard[k])]]);
+                        T* grow = Gk + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {
                             if (!vok[v]) continue;

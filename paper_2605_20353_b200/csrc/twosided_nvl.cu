@@ -313,3 +313,120 @@ gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower) {
 }
 
 }  // namespace gcp
+
+namespace gcp {
+
+// ---- two-sided by peer access (GCP_TWOSIDED_NVL=peer) ---------------------
+// K2 itself reaches every row owned elsewhere: it gathers the row from the
+// owner's A window and scatter-adds its contribution into the owner's G
+// window (red.global.add over NVLink), so only the touched rows cross the link
+// -- the paper's import and export, fused into the sampling kernel -- and no
+// touch pass, bitmap or copy is needed.  The step kernel then has every owner
+// update its rows between two LSA barriers.
+bool tsn_peer_wanted() {
+    const char* env = getenv("GCP_TWOSIDED_NVL");
+    return env && std::string(env) == "peer";
+}
+
+__global__ void k_tsn_bases(ncclDevComm comm, ncclWindow_t winA, ncclWindow_t winG0, ncclWindow_t winG1, int P,
+                            void** out) {
+    const int r = threadIdx.x;
+    if (r >= P) return;
+    out[r] = ncclGetLsaPointer(winA, 0, r);
+    out[8 + r] = ncclGetLsaPointer(winG0, 0, r);
+    out[16 + r] = ncclGetLsaPointer(winG1, 0, r);
+}
+
+gcp_status tsn_peer_setup(gcp_ctx* c) {
+    if (c->P > 8) return set_error(GCP_E_ARG, "two-sided peer access: at most 8 ranks");
+    TSN_CUDA(c, gmalloc(c, &c->d_peer_bases, 24 * sizeof(void*)), "peer bases");
+    TSN_CUDA(c, cudaMemsetAsync(c->d_peer_bases, 0, 24 * sizeof(void*), c->stream), "peer bases");
+    k_tsn_bases<<<1, 32, 0, c->stream>>>(c->devcomm, c->winA, c->winG[0], c->winG[1], c->P, c->d_peer_bases);
+    TSN_CUDA(c, cudaGetLastError(), "peer bases");
+    c->launches++;
+    c->tsn_peer = true;
+    return GCP_OK;
+}
+
+// barrier (every member's K2 -- and so every red.add into my G rows -- is
+// complete); Alg. 1 on my owned rows of the current G; the other G parity
+// cleared (no member adds into it before the next barrier); barrier (every
+// owner's rows are updated before any next K2 gathers them)
+template <typename T>
+__global__ void __launch_bounds__(512) k_tsn_peer_step(ncclDevComm comm, T* __restrict__ A, const T* __restrict__ G,
+                                                       T* __restrict__ Gnext, int64_t n_coef, T* __restrict__ B,
+                                                       T* __restrict__ C, const TsnArgs ta, T rate, T b1, T b2,
+                                                       T eps, T bc1, T bc2, T lower, const DevStep* step,
+                                                       long long t_off) {
+    using V = typename TVec<T>::type;
+    constexpr int VE = TVec<T>::n;
+    if (step) {
+        const double t = (double)(step->t + t_off);
+        rate = (T)step->rate;
+        bc1 = (T)(1.0 / (1.0 - pow(step->beta1, t)));
+        bc2 = (T)(1.0 / (1.0 - pow(step->beta2, t)));
+    }
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamLsa(comm), comm.lsaBarrier, blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    V z;
+    T* zp = reinterpret_cast<T*>(&z);
+#pragma unroll
+    for (int q = 0; q < VE; ++q) zp[q] = T(0);
+    for (int64_t x = tid; x < n_coef / VE; x += nt) reinterpret_cast<V*>(Gnext)[x] = z;
+    for (int k = 0; k < ta.d; ++k) {
+        const int64_t e0 = ta.off[k] + (int64_t)ta.me[k] * ta.shard[k] * ta.R_pad;
+        const int64_t nv = ta.shard[k] * ta.R_pad / VE;
+        for (int64_t v = tid; v < nv; v += nt) {
+            const int64_t e = e0 + v * VE;
+            V g = *reinterpret_cast<const V*>(G + e);
+            V a = *reinterpret_cast<const V*>(A + e);
+            V bb = *reinterpret_cast<const V*>(B + e);
+            V cc = *reinterpret_cast<const V*>(C + e);
+            const T* gp = reinterpret_cast<const T*>(&g);
+            T* ap = reinterpret_cast<T*>(&a);
+            T* bp = reinterpret_cast<T*>(&bb);
+            T* cp = reinterpret_cast<T*>(&cc);
+#pragma unroll
+            for (int q = 0; q < VE; ++q) {
+                const T gv = gp[q];
+                bp[q] = b1 * bp[q] + (T(1) - b1) * gv;
+                cp[q] = b2 * cp[q] + (T(1) - b2) * gv * gv;
+                const T av = ap[q] - rate * ((bp[q] * bc1) / sqrt(cp[q] * bc2 + eps));
+                ap[q] = (av < lower) ? lower : av;
+            }
+            *reinterpret_cast<V*>(A + e) = a;
+            *reinterpret_cast<V*>(B + e) = bb;
+            *reinterpret_cast<V*>(C + e) = cc;
+        }
+    }
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+gcp_status tsn_peer_step(gcp_ctx* c, const gcp_adam_params* p, double lower) {
+    const TsnArgs ta = tsn_args(c);
+    const int cur = (int)(c->it & 1);
+    void* G = cur ? c->d_G2 : c->d_G;
+    void* Gn = cur ? c->d_G : c->d_G2;
+    const double bc1 = 1.0 / (1.0 - pow(p->beta1, (double)c->t));
+    const double bc2 = 1.0 / (1.0 - pow(p->beta2, (double)c->t));
+    const DevStep* step = c->capturing ? c->d_step : nullptr;
+    const long long toff = (long long)(c->t - c->graph_t0);
+    cudaEvent_t ev;
+    prof_begin(c, PROF_COMM, &ev);
+    if (c->prec == GCP_FP32)
+        k_tsn_peer_step<float><<<c->fused_ctas, 512, 0, c->stream>>>(
+            c->devcomm, (float*)c->d_A, (const float*)G, (float*)Gn, c->n_coef, (float*)c->d_B, (float*)c->d_C, ta,
+            (float)p->rate, (float)p->beta1, (float)p->beta2, (float)p->eps, (float)bc1, (float)bc2, (float)lower,
+            step, toff);
+    else
+        k_tsn_peer_step<double><<<c->fused_ctas, 512, 0, c->stream>>>(
+            c->devcomm, (double*)c->d_A, (const double*)G, (double*)Gn, c->n_coef, (double*)c->d_B, (double*)c->d_C,
+            ta, p->rate, p->beta1, p->beta2, p->eps, bc1, bc2, lower, step, toff);
+    TSN_CUDA(c, cudaGetLastError(), "two-sided peer step");
+    c->launches += 1;
+    prof_end(c, PROF_COMM, ev);
+    return GCP_OK;
+}
+
+}  // namespace gcp

@@ -33,6 +33,9 @@ def main():
     if mode == "twosided_nccl":
         os.environ["GCP_TWOSIDED_NVL"] = "0"   # the NCCL send/recv two-sided path (twosided.cu)
         mode = "twosided"
+    if mode == "twosided_peer":
+        os.environ["GCP_TWOSIDED_NVL"] = "peer"   # K2 reaches the owners' rows over NVLink (twosided_nvl.cu)
+        mode = "twosided"
     mode = "sync" if mode == "sync32" else mode
     # TG, TE: the C18 bounds (gradient per element vs the rounding scale S, loss
     # estimate vs sum |terms|) from an identical state.  TM / TM_FIT / TE_FIT bound

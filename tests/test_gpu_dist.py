@@ -17,7 +17,8 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("nproc", [2, 4])
-@pytest.mark.parametrize("mode", ["sync", "sync32", "twosided", "twosided_nccl", "async", "fedadam"])
+@pytest.mark.parametrize("mode", ["sync", "sync32", "twosided", "twosided_nccl", "twosided_peer", "async",
+                                  "fedadam"])
 def test_multi_gpu_parity(mode, nproc):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
