@@ -33,7 +33,8 @@ def main():
     if mode == "twosided_nccl":
         os.environ["GCP_TWOSIDED_NVL"] = "0"   # the NCCL send/recv two-sided path (twosided.cu)
         mode = "twosided"
-    if mode == "twosided_peer":
+    peer = mode == "twosided_peer"
+    if peer:
         os.environ["GCP_TWOSIDED_NVL"] = "peer"   # K2 reaches the owners' rows over NVLink (twosided_nvl.cu)
         mode = "twosided"
     mode = "sync" if mode == "sync32" else mode
@@ -94,9 +95,23 @@ def main():
             pw, qw = oracle.local_counts(mine, p, q, ws, rank)
             Go, S, _ = oracle.sampled_grad(mine, A_rank, loss, seed, rank, it, pw, qw)
             ctx.loss_grad(loss)
+            if peer:
+                # peer access: every contribution to a row lands in its owner's G,
+                # so a rank holds the global (all-rank) gradient of its owned rows
+                Gs, Ss, _ = oracle.sync_gradient(blocks, A_rank, loss, seed, it, p, q)
             for k in range(3):
                 Gg = ctx.grad_get(k)
-                assert np.all(np.abs(Gg - Go[k]) <= TG * S[k] + 1e-300), f"grad it={it} k={k}"
+                if peer:
+                    gk = math.prod(grid) // grid[k]
+                    rows_k = -(-(-(-dims[k] // grid[k])) // gk) * gk
+                    sh = rows_k // gk
+                    me = [w for w in oracle.slice_groups(grid, k) if rank in w][0].index(rank)
+                    o0, o1 = me * sh, min((me + 1) * sh, mine.hi[k] - mine.lo[k])
+                    want = Gs[k][mine.lo[k] + o0: mine.lo[k] + o1]
+                    sc = Ss[k][mine.lo[k] + o0: mine.lo[k] + o1]
+                    assert np.all(np.abs(Gg[o0:o1] - want) <= TG * sc + 1e-300), f"owned grad it={it} k={k}"
+                else:
+                    assert np.all(np.abs(Gg - Go[k]) <= TG * S[k] + 1e-300), f"grad it={it} k={k}"
         else:
             ctx.loss_grad(loss)
         ctx.adam_step(ap)
