@@ -118,6 +118,32 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 20 ms"}
 
 
+def nvlink_counters(dev):
+    """NVLink data bytes this GPU has sent / received so far, summed over its
+    links, from NVML's per-link NVLink counters (tools/nvlink_probe.py checks
+    the fields against a peer copy of known size).  None when NVML has none."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(dev_index(dev))
+        out = {}
+        for name, fid, scale in (("tx", nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 1024),
+                                 ("rx", nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024)):
+            tot, nlinks = 0, 0
+            for link in range(18):
+                fv = nv.nvmlDeviceGetFieldValues(h, [(fid, link)])[0]
+                if fv.nvmlReturn == 0:
+                    tot += int(fv.value.ullVal) * scale
+                    nlinks += 1
+            if not nlinks:
+                return None
+            out[name] = tot
+        out["links"] = nlinks
+        return out
+    except Exception:
+        return None
+
+
 def dev_index(local):
     """Physical index of the local CUDA device (honours CUDA_VISIBLE_DEVICES)."""
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -400,12 +426,14 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier(ws)
     torch.cuda.synchronize()
+    nvl0 = nvlink_counters(dev) if ws > 1 else None
     with ClockSampler(dev) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             ctx.fit_epoch()
         ev1.record(stream)
         torch.cuda.synchronize()
+    nvl1 = nvlink_counters(dev) if ws > 1 else None
     barrier(ws)
     ms_local = ev0.elapsed_time(ev1)
     ms = allmax(ws, ms_local)
@@ -423,6 +451,15 @@ def main():
     prof_ranks = allgather_obj(ws, {k: v[0] / prof_epochs for k, v in prof.items()})
     ms_step = ms / args.steps
     eps = 1000.0 / ms_step
+    nvlink = None
+    if nvl0 and nvl1:
+        per = {k: (nvl1[k] - nvl0[k]) / (args.steps * ITERS) for k in ("tx", "rx")}
+        nvlink = {"ranks_bytes_per_iter": allgather_obj(ws, per), "links": nvl1["links"],
+                  "source": "NVML NVLink data counters (THROUGHPUT_DATA_TX/RX, KiB, summed over links) "
+                            "read on each rank just before and after the timed region; per iteration = "
+                            "delta / (steps x iters_per_epoch), includes the loss estimate's scalar sums",
+                  "alg_bytes_per_iter_rank": exchange_alg_bytes(w, grid, args.mode, args.tau,
+                                                                4 if args.precision == "fp32" else 8)}
     samples_per_s = eps * ITERS * (2 * w["s"])
     # library kernels in the timed region: launch counter delta, minus NCCL collective
     # calls (the fused NVLink exchange is a library kernel and stays counted)
@@ -483,6 +520,7 @@ def main():
             "phase_ms_per_step_ranks": prof_ranks if ws > 1 else None,
             "phase_source": f"library CUDA events over {prof_epochs} extra untimed epochs (rank 0)",
             "roofline": roof,
+            "nvlink": nvlink,
             "hbm_gate": gate,
             "clocks": clocks,
             "e2e": e2e,
@@ -493,6 +531,28 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def exchange_alg_bytes(w, grid, mode, tau, esz):
+    """Algorithmic NVLink bytes one rank sends per iteration in the multi-GPU
+    exchange: sync (fused RS + Adam + AG over a slice group of
+    g_k = P / N_k ranks) -- the peers pull (g_k - 1) / g_k of this rank's G block
+    and it stores its 1/g_k shard of A into g_k - 1 peers: 2 (g_k - 1) / g_k of
+    the mode's block bytes; async -- one all-reduce of the block every tau
+    iterations, ~2 (g_k - 1) / g_k of it; two-sided -- data dependent (None)."""
+    P = int(np.prod(grid))
+    R_pad = (w["R"] + 3) // 4 * 4
+    tot = 0.0
+    for k, n_k in enumerate(grid):
+        g = P // n_k
+        rows = -(-w["dims"][k] // n_k)
+        if g > 1:
+            tot += 2 * (g - 1) / g * rows * R_pad * esz
+    if mode == "sync":
+        return tot
+    if mode in ("async", "fedadam"):
+        return tot / max(tau, 1)
+    return None
 
 
 def ncu_traffic(name, layout):

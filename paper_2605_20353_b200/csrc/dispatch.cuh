@@ -7,10 +7,10 @@
 
 namespace gcp {
 
-template <typename T, int D, int GL, int NV>
+template <typename T, int D, int GL, int NV, int VAR>
 static cudaError_t run_sample(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, const KParams<T>& kp,
                               int nblocks) {
-    k_sample<T, D, GL, NV><<<nblocks, kBlock, 0, c->stream>>>(s, m, kp);
+    k_sample<T, D, GL, NV, VAR><<<nblocks, kBlock, 0, c->stream>>>(s, m, kp);
     return cudaGetLastError();
 }
 
@@ -43,17 +43,20 @@ static auto mode_switch(int d, int nvec, F&& f) {
     }
 }
 
+template <int VAR>
 struct SampleLaunch {
     gcp_ctx* c; const SampleArgs* s; const ModelArgs* m; const void* kp; int nblocks;
     template <typename T, int D, int GL, int NV> cudaError_t operator()() const {
-        return run_sample<T, D, GL, NV>(c, *s, *m, *static_cast<const KParams<T>*>(kp), nblocks);
+        return run_sample<T, D, GL, NV, VAR>(c, *s, *m, *static_cast<const KParams<T>*>(kp), nblocks);
     }
 };
 struct SampleOcc {
     template <typename T, int D, int GL, int NV> int operator()() const { return occ_sample<T, D, GL, NV>(); }
 };
 
-template <typename T>
+// one K2 launch of variant VAR (kernels_f32.cu / kernels_f64.cu instantiate the
+// plain kernel, kernels_var.cu the peer-access and warp-aggregated ones)
+template <typename T, int VAR>
 cudaError_t sample_kernel_T(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss, int loss_mode,
                             int semi_nz, double w_nz, double w_z, int with_loss, double* partials,
                             int nblocks, const OrdHistArgs* oh) {
@@ -63,7 +66,7 @@ cudaError_t sample_kernel_T(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m,
     kp.loss = loss; kp.loss_mode = loss_mode; kp.semi_nz = semi_nz; kp.with_loss = with_loss;
     kp.w_nz = (T)w_nz; kp.w_z = (T)w_z; kp.partials = partials;
     const int nvec = m.R_pad / Vec16<T>::n;
-    return mode_switch<T>(c->d, nvec, SampleLaunch{c, &s, &m, &kp, nblocks});
+    return mode_switch<T>(c->d, nvec, SampleLaunch<VAR>{c, &s, &m, &kp, nblocks});
 }
 
 template <typename T>

@@ -13,6 +13,14 @@ cudaError_t sample_kernel_f32(gcp_ctx*, const SampleArgs&, const ModelArgs&, int
                               int, double*, int, const OrdHistArgs*);
 cudaError_t sample_kernel_f64(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
                               int, double*, int, const OrdHistArgs*);
+cudaError_t sample_kernel_peer_f32(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
+                              int, double*, int, const OrdHistArgs*);
+cudaError_t sample_kernel_peer_f64(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
+                              int, double*, int, const OrdHistArgs*);
+cudaError_t sample_kernel_wagg_f32(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
+                              int, double*, int, const OrdHistArgs*);
+cudaError_t sample_kernel_wagg_f64(gcp_ctx*, const SampleArgs&, const ModelArgs&, int, int, int, double, double,
+                              int, double*, int, const OrdHistArgs*);
 int sample_occupancy_f32(int, int);
 int sample_occupancy_f64(int, int);
 cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
@@ -34,6 +42,18 @@ int sample_kernel_blocks(gcp_ctx* c) {
 cudaError_t launch_sample_kernel(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss, int loss_mode,
                                  int semi_nz, double w_nz, double w_z, int with_loss, double* partials,
                                  int nblocks, const OrdHistArgs* oh) {
+    // K2 variant: rows owned elsewhere (two-sided by peer access) -> kVarPeer;
+    // GCP_WAGG=1 -> warp-aggregated scatter-adds (gradient launches only)
+    const char* we = getenv("GCP_WAGG");
+    const int var = m.peerA ? kVarPeer : (!loss_mode && we && we[0] == '1') ? kVarWagg : kVarPlain;
+    if (var == kVarPeer)
+        return c->prec == GCP_FP32
+                   ? sample_kernel_peer_f32(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh)
+                   : sample_kernel_peer_f64(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh);
+    if (var == kVarWagg)
+        return c->prec == GCP_FP32
+                   ? sample_kernel_wagg_f32(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh)
+                   : sample_kernel_wagg_f64(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh);
     return c->prec == GCP_FP32
                ? sample_kernel_f32(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh)
                : sample_kernel_f64(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nblocks, oh);

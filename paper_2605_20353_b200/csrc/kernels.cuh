@@ -108,7 +108,13 @@ __device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t s, int64
     return v;
 }
 
-template <typename T, int D, int GL, int NV>
+// K2 variants, one instantiation each so the default carries neither branch:
+// kVarPlain; kVarPeer -- rows owned by other ranks are gathered from / added into
+// their A / G windows over NVLink (two-sided by peer access); kVarWagg -- same-row
+// scatter-adds of a round aggregated in registers (GCP_WAGG=1)
+enum { kVarPlain = 0, kVarPeer = 1, kVarWagg = 2 };
+
+template <typename T, int D, int GL, int NV, int VAR = kVarPlain>
 __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
                                                    const KParams<T> kp) {
     constexpr int VE = Vec16<T>::n;
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                 for (int k = 0; k < D; ++k) {
                     GCP_CHECK(!(rf[b] & 1) || rc[b][k] < sa.bdim[k], "gather row", rc[b][k], sa.bdim[k]);
                     const T* Ak = A;
-                    if (ma.peerA && ma.nmem[k] > 1)   // the owner's A window (peer access over NVLink)
+                    if (VAR == kVarPeer && ma.nmem[k] > 1)   // the owner's A window (peer access over NVLink)
                         Ak = static_cast<const T*>(ma.peerA[ma.mem[k][(int)(rc[b][k] / (uint64_t)ma.shard[k])]]);
                     const T* row = Ak + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
@@ -219,17 +225,30 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                 if (kp.semi_nz && isnz) y = rw[b] * (loss_df<T>(kp.loss, rx[b], m) - loss_df<T>(kp.loss, T(0), m));
                 else y = rw[b] * loss_df<T>(kp.loss, rx[b], m);
                 if (kp.with_loss && ok && gl == 0) lacc += (double)(rw[b] * loss_f<T>(kp.loss, rx[b], m));
-                if (!kp.loss_mode && ok) {
+                if (!kp.loss_mode) {
 #pragma unroll
                     for (int k = 0; k < D; ++k) {
-                        GCP_CHECK(rc[b][k] < sa.bdim[k], "scatter row", rc[b][k], sa.bdim[k]);
+                        // warp aggregation (kVarWagg, north star / P:591-598): the
+                        // samples of this round that hit the same row of mode k add
+                        // their contributions in registers and the lowest such group
+                        // issues one red.add; cost 1 match + 1 vote when no row repeats
+                        bool lead = ok, dup = false;
+                        uint32_t key = ok ? rc[b][k] : 0xFFFFFFFFu;
+                        if (VAR == kVarWagg) {
+                            constexpr uint32_t pat = 0xFFFFFFFFu / (uint32_t)((1ull << GL) - 1);
+                            const uint32_t peers = __match_any_sync(0xffffffffu, key) & (pat << gl);
+                            dup = __any_sync(0xffffffffu, ok && __popc(peers) > 1);
+                            lead = ok && (__ffs(peers) - 1 == lane);
+                        }
+                        if (!dup && !ok) continue;
+                        GCP_CHECK(!ok || rc[b][k] < sa.bdim[k], "scatter row", rc[b][k], sa.bdim[k]);
                         T* Gk = G;
-                        if (ma.peerA && ma.nmem[k] > 1)   // the owner's G window: red.add over NVLink
+                        if (VAR == kVarPeer && ma.nmem[k] > 1)   // the owner's G window: red.add over NVLink
                             Gk = static_cast<T*>(ma.peerG[ma.mem[k][(int)(rc[b][k] / (uint64_t)ma.shard[k])]]);
                         T* grow = Gk + ma.off[k] + (int64_t)rc[b][k] * ma.row_stride;
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {
-                            if (!vok[v]) continue;
+                            if (!vok[v] && !dup) continue;   // (a dup round keeps every lane in the shuffles)
                             T cv[VE];
 #pragma unroll
                             for (int e = 0; e < VE; ++e) {
@@ -239,7 +258,20 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                                     if (j != k) z *= a[b][j][v][e];
                                 cv[e] = z;
                             }
-                            red_add_v(grow + (gl + v * GL) * VE, cv);
+                            if (dup) {   // rare: sum the other groups' vectors of the same row
+#pragma unroll
+                                for (int j = 1; j < SPR; ++j) {
+                                    const int srcl = (lane + j * GL) & 31;
+                                    const uint32_t ok2 = __shfl_sync(0xffffffffu, key, srcl);
+                                    T o[VE];
+#pragma unroll
+                                    for (int e = 0; e < VE; ++e) o[e] = __shfl_sync(0xffffffffu, cv[e], srcl);
+                                    if (ok2 == key)
+#pragma unroll
+                                        for (int e = 0; e < VE; ++e) cv[e] += o[e];
+                                }
+                            }
+                            if (lead && vok[v]) red_add_v(grow + (gl + v * GL) * VE, cv);
                         }
                     }
                 }

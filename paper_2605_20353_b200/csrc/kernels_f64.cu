@@ -5,7 +5,7 @@ namespace gcp {
 cudaError_t sample_kernel_f64(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss, int loss_mode,
                             int semi_nz, double w_nz, double w_z, int with_loss, double* partials, int nb,
                             const OrdHistArgs* oh) {
-    return sample_kernel_T<double>(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nb, oh);
+    return sample_kernel_T<double, kVarPlain>(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nb, oh);
 }
 int sample_occupancy_f64(int d, int R_pad) { return sample_occupancy_T<double>(d, R_pad); }
 cudaError_t export_f64(gcp_ctx* c, const SampleArgs& s, int64_t first, int64_t count, const int64_t* lo,

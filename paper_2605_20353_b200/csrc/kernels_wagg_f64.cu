@@ -1,0 +1,12 @@
+// kernels_wagg_f64.cu -- instantiation of the K2 warp-aggregated scatter-add variant (kernels.cuh)
+// for T = double; one translation unit per (variant, type) so they compile in
+// parallel with the plain kernels (kernels_f32.cu / kernels_f64.cu).
+#include "dispatch.cuh"
+
+namespace gcp {
+cudaError_t sample_kernel_wagg_f64(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m, int loss, int loss_mode,
+                                  int semi_nz, double w_nz, double w_z, int with_loss, double* partials, int nb,
+                                  const OrdHistArgs* oh) {
+    return sample_kernel_T<double, kVarWagg>(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nb, oh);
+}
+}  // namespace gcp

@@ -173,6 +173,33 @@ def test_slot_order_same_gradient(gcp, orc, strategy, prec, tiles, monkeypatch):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("R", [4, 10, 16, 40])
+@pytest.mark.parametrize("order", ["0", "1"])
+def test_warp_aggregated_scatter_same_gradient(gcp, orc, prec, R, order, monkeypatch):
+    """GCP_WAGG=1: the samples of a K2 round that hit the same row of a mode
+    sum their contributions in registers (__match_any_sync) and one group
+    issues the red.add (P:591-598's atomic MTTKRP, aggregated).  20/30/40 rows
+    make repeats frequent (R = 4: 32 samples per round); R = 10 leaves a lane
+    of every group without a vector (the shuffles must still include it);
+    R = 40 two vectors per lane.  Same samples, so the oracle's gradient within
+    the C18 tolerance, slot order on and off."""
+    monkeypatch.setenv("GCP_WAGG", "1")
+    monkeypatch.setenv("GCP_SLOT_ORDER", order)
+    dims = (20, 30, 40)
+    subs, vals = _tensor("poisson")
+    c = _ctx(gcp, dims, subs, vals, prec=prec, R=R)
+    t = orc.Tensor(dims, subs, vals)
+    for it, (p, q) in enumerate([(1000, 1000), (3333, 77)]):
+        c.sample("stratified", p, q, 3001)
+        A = _model(c, 3)
+        c.loss_grad("poisson")
+        G = [c.grad_get(k) for k in range(3)]
+        Go, S, _ = orc.sampled_grad(t, A, "poisson", 3001, 0, it, p, q, "stratified")
+        _grad_check(G, Go, S, TOL[prec], f"wagg R={R} {prec} order={order} p={p} q={q}")
+        c.adam_step(gcp.adam_params(rate=1e-2))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
 @pytest.mark.parametrize("loss", LOSSES)
 def test_loss_estimate_parity(gcp, orc, loss, prec):
     dims = (20, 30, 40)

@@ -1,0 +1,75 @@
+"""Which NVML NVLink byte counters move on this pool's B200s, and by how much.
+
+One process, two GPUs: a known number of bytes is copied GPU0 -> GPU1 (peer
+copy over NVLink); the NVML field values of every link are read before and
+after on both GPUs and the deltas printed next to the copied bytes.  bench.py
+uses the field that reports the copy faithfully to count the NVLink bytes of
+the multi-GPU exchange in its timed region.
+"""
+import json
+import sys
+
+import pynvml as nv
+import torch
+
+FIELDS = {
+    "THROUGHPUT_DATA_TX": nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+    "THROUGHPUT_DATA_RX": nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
+    "THROUGHPUT_RAW_TX": nv.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX,
+    "THROUGHPUT_RAW_RX": nv.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX,
+    "COUNT_XMIT_BYTES": nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES,
+    "COUNT_RCV_BYTES": nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES,
+}
+NLINK = 18
+
+
+def read(h):
+    out = {}
+    for name, fid in FIELDS.items():
+        vals = []
+        for link in list(range(NLINK)) + [0xFFFFFFFF]:
+            try:
+                fv = nv.nvmlDeviceGetFieldValues(h, [(fid, link)])[0]
+                if fv.nvmlReturn != 0:
+                    vals.append(None)
+                    continue
+                vt = fv.valueType
+                v = {0: fv.value.dVal, 1: fv.value.uiVal, 2: fv.value.ulVal, 3: fv.value.ullVal,
+                     4: fv.value.sllVal}.get(vt, fv.value.ullVal)
+                vals.append(int(v))
+            except Exception as e:  # noqa: BLE001
+                vals.append(None)
+        out[name] = vals
+    return out
+
+
+def delta(a, b):
+    return {k: [(y - x) if (x is not None and y is not None) else None for x, y in zip(a[k], b[k])] for k in a}
+
+
+def main():
+    nv.nvmlInit()
+    n = torch.cuda.device_count()
+    hs = [nv.nvmlDeviceGetHandleByIndex(i) for i in range(n)]
+    nbytes = int(float(sys.argv[1]) if len(sys.argv) > 1 else 4e9)
+    src = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda:0").fill_(1.0)
+    dst = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda:1")
+    dst.copy_(src)
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    before = [read(h) for h in hs[:2]]
+    reps = 5
+    for _ in range(reps):
+        dst.copy_(src)
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    after = [read(h) for h in hs[:2]]
+    res = {"copied_bytes": nbytes * reps, "direction": "gpu0 -> gpu1",
+           "delta_gpu0": delta(before[0], after[0]), "delta_gpu1": delta(before[1], after[1])}
+    for g in ("delta_gpu0", "delta_gpu1"):
+        res[g + "_sum_links"] = {k: sum(x for x in v[:NLINK] if x is not None) for k, v in res[g].items()}
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
