@@ -184,6 +184,7 @@ SampleArgs sample_args(const gcp_ctx* c, int64_t p, int64_t q, uint64_t seed, ui
     s.err_slot = c->d_err;
     s.it_dev = nullptr;
     s.order = nullptr;
+    s.l2_first = c->l2_first;
     if (c->capturing) {   // epoch graph: this launch's iteration relative to the replay's first
         s.it_dev = &c->d_step->it;
         s.it = it - c->graph_it0;
@@ -667,6 +668,12 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
         const char* env = getenv("GCP_AG_INTERLEAVE");
         if (env) il = atoi(env) != 0 && c->P == 1 && c->mode == GCP_DIST_SYNC;
         c->ag_interleaved = il;
+        // the records and hash buckets K2 reads once per sample take an L2
+        // evict_first policy when the factors spill out of L2, so they do not
+        // displace reused factor rows (c4 K2 2.665 -> 2.62 ms; with L2-resident
+        // factors it costs c2 ~1%, profiles/r02l_*); GCP_L2_HINT=0/1 overrides
+        const char* hv = getenv("GCP_L2_HINT");
+        c->l2_first = hv ? atoi(hv) != 0 : spills;
         c->ag_stride = il ? 2 * c->R_pad : c->R_pad;
         // slot ordering by mode-1 position: pays when mode 1's A and G rows
         // themselves spill out of L2 (c4, c5); GCP_SLOT_ORDER=0/1 overrides

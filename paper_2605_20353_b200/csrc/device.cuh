@@ -185,6 +185,19 @@ __device__ __forceinline__ uint64_t first_bucket(const SampleArgs& a, const uint
     return 2 * ((hash_key(klo, khi) & a.hash_mask) & ~1ull);
 }
 
+// 16-B read of a line used once (record, hash bucket): with l2_first an L2
+// evict_first cache policy so it does not displace the reused factor rows
+__device__ __forceinline__ uint4 ldg_once(const uint4* p, int l2_first) {
+    if (!l2_first) return __ldg(p);
+    uint4 v;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 template <typename T, int D>
 __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t s) {
     Pending<D> P;
@@ -198,8 +211,8 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
         const uint64_t j = range_map(w.w0, (uint64_t)a.N);
         GCP_CHECK(j < (uint64_t)a.N || a.rec_words == 0, "record index >= N", j, a.N);
         const uint4* r = reinterpret_cast<const uint4*>(a.rec + j * a.rec_words);
-        P.w0 = __ldg(r);
-        if (VW + D > 4) P.w1 = __ldg(r + 1);
+        P.w0 = ldg_once(r, a.l2_first);
+        if (VW + D > 4) P.w1 = ldg_once(r + 1, a.l2_first);
         P.slot = (uint32_t)s;
         P.j = (uint32_t)j;
         P.state = 1;
@@ -227,8 +240,8 @@ __device__ __forceinline__ Pending<D> issue_sample(const SampleArgs& a, int64_t 
     }
     GCP_CHECK(b + 4 <= (a.hash_mask + 1) * (a.key128 ? 2 : 1), "hash bucket past the table", b, a.hash_mask);
     const uint4* h = reinterpret_cast<const uint4*>(a.hash + b);
-    P.w0 = __ldg(h);
-    P.w1 = __ldg(h + 1);
+    P.w0 = ldg_once(h, a.l2_first);
+    P.w1 = ldg_once(h + 1, a.l2_first);
     P.state = 2;
     return P;
 }

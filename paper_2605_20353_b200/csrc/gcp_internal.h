@@ -71,6 +71,7 @@ struct SampleArgs {
     const uint64_t* filter;   // blocked Bloom filter of the block's keys (4 u64 per 32-B sector), or null
     uint64_t filter_mask;     // sectors - 1 (power of two)
     const uint32_t* order;    // gradient launches: slot processing order (null = slot order), see slot_order
+    int l2_first;             // 1: record and hash-bucket reads (used once) carry an L2 evict_first policy
 };
 
 // Epoch-graph replay state: the values of rate, t and it at the start of the
@@ -205,6 +206,7 @@ struct gcp_ctx {
     int64_t rows[gcp::kMaxModes] = {0};     // allocated rows per mode (>= block rows, multiple of slice size)
     int64_t off[gcp::kMaxModes] = {0};      // element offsets
     int64_t n_coef = 0;                     // logical coefficients (B, C layout)
+    int l2_first = 0;                       // K2's record / bucket reads carry an L2 evict_first policy
     bool ag_interleaved = false;            // A and G rows interleaved in one buffer (d_G = d_A + R_pad)
     int ag_stride = 0;                      // elements between consecutive A (or G) rows
     void *d_A = nullptr, *d_G = nullptr, *d_B = nullptr, *d_C = nullptr, *d_lambda = nullptr;

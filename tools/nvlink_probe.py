@@ -21,6 +21,7 @@ FIELDS = {
     "COUNT_RCV_BYTES": nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES,
 }
 NLINK = 18
+ERRS = {}
 
 
 def read(h):
@@ -32,6 +33,7 @@ def read(h):
                 fv = nv.nvmlDeviceGetFieldValues(h, [(fid, link)])[0]
                 if fv.nvmlReturn != 0:
                     vals.append(None)
+                    ERRS.setdefault(name, set()).add(int(fv.nvmlReturn))
                     continue
                 vt = fv.valueType
                 v = {0: fv.value.dVal, 1: fv.value.uiVal, 2: fv.value.ulVal, 3: fv.value.ullVal,
@@ -41,6 +43,13 @@ def read(h):
                 vals.append(None)
         out[name] = vals
     return out
+
+
+def smi():
+    import subprocess
+    r = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", "0"], capture_output=True, text=True)
+    r1 = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", "1"], capture_output=True, text=True)
+    return r.stdout + r.stderr, r1.stdout + r1.stderr
 
 
 def delta(a, b):
@@ -58,16 +67,27 @@ def main():
     torch.cuda.synchronize(0)
     torch.cuda.synchronize(1)
     before = [read(h) for h in hs[:2]]
+    smi0 = smi()
     reps = 5
     for _ in range(reps):
         dst.copy_(src)
     torch.cuda.synchronize(0)
     torch.cuda.synchronize(1)
     after = [read(h) for h in hs[:2]]
+    smi1 = smi()
     res = {"copied_bytes": nbytes * reps, "direction": "gpu0 -> gpu1",
            "delta_gpu0": delta(before[0], after[0]), "delta_gpu1": delta(before[1], after[1])}
     for g in ("delta_gpu0", "delta_gpu1"):
         res[g + "_sum_links"] = {k: sum(x for x in v[:NLINK] if x is not None) for k, v in res[g].items()}
+    res["nvml_errors"] = {k: sorted(v) for k, v in ERRS.items()}
+    st = []
+    for link in range(NLINK):
+        try:
+            st.append(int(nv.nvmlDeviceGetNvLinkState(hs[0], link)))
+        except Exception as e:  # noqa: BLE001
+            st.append(str(e))
+    res["nvlink_state_gpu0"] = st
+    res["smi_before"], res["smi_after"] = smi0, smi1
     print(json.dumps(res))
 
 
