@@ -503,8 +503,7 @@ def main():
             "config": {"workload": f"{name}: {w['desc']}", "dims": list(w["dims"]), "nnz": int(w["nnz"]),
                        "R": w["R"], "loss": w["loss"], "p": w["s"], "q": w["s"], "f_nz": w["f"], "f_z": w["f"],
                        "iters_per_epoch": ITERS, "grid": list(grid), "dist_mode": args.mode,
-                       "exchange": ("none" if ws == 1 else "fused-nvlink-multimem" if features["multimem"]
-                                    else "fused-nvlink" if features["fused"] else "nccl"),
+                       "exchange": exchange_name(ws, args.mode, features),
                        "parallelism": f"grid{'x'.join(map(str, grid))}-{args.mode}" if ws > 1 else "single-gpu",
                        "l2": ("inputs larger than L2 (COO records + hash set >> 126 MB); factors "
                               + ("stay L2-resident" if sum(w["dims"]) * w["R"] * 4 < 32e6
@@ -520,7 +519,7 @@ def main():
             "phase_ms_per_step_ranks": prof_ranks if ws > 1 else None,
             "phase_source": f"library CUDA events over {prof_epochs} extra untimed epochs (rank 0)",
             "roofline": roof,
-            "nvlink": nvlink,
+            **({"nvlink": nvlink} if nvlink else {}),
             "hbm_gate": gate,
             "clocks": clocks,
             "e2e": e2e,
@@ -531,6 +530,21 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def exchange_name(ws, mode, features):
+    if ws == 1:
+        return "none"
+    if mode == "twosided":
+        env = os.environ.get("GCP_TWOSIDED_NVL")
+        if not features["fused"]:
+            return "two-sided-nccl-send-recv"
+        if env == "peer" or (env is None and ws <= 8):
+            return "two-sided-nvlink-peer-access"
+        return "two-sided-nvlink-import-export"
+    if mode in ("async", "fedadam"):
+        return "nccl-allreduce-every-tau"
+    return "fused-nvlink-multimem" if features["multimem"] else "fused-nvlink" if features["fused"] else "nccl"
 
 
 def exchange_alg_bytes(w, grid, mode, tau, esz):

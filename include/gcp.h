@@ -84,7 +84,10 @@ typedef enum {
     GCP_DIST_ASYNC_AVG = 1,       /* LocalSGD averaging every tau iterations (Alg. 3) */
     GCP_DIST_ASYNC_FEDADAM = 2,   /* FedAdam server step every tau iterations (Alg. 4) */
     GCP_DIST_SYNC_TWO_SIDED = 3   /* "two-sided" layout: rows partitioned, per-iteration import/export;
-                                     gcp_model_get and gcp_loss_estimate are collective in this mode */
+                                     gcp_model_get and gcp_loss_estimate are collective in this mode.  Within one
+                                     NVLink domain of <= 8 ranks the gradient kernel reaches the owners' rows by
+                                     peer access (environment GCP_TWOSIDED_NVL=1: import/export kernels over
+                                     NVLink windows; =0: NCCL send/recv) */
 } gcp_dist_mode;
 
 /* Alg. 1 hyper-parameters.  lower: NaN selects the loss default. */
@@ -271,7 +274,7 @@ gcp_status gcp_loss_estimate(gcp_ctx* ctx, gcp_loss loss, int64_t f_nz, int64_t 
  * *done_out = 1 when fails reached max_fails or the epoch budget is spent.
  * On a non-legacy stream the epoch's iterations are captured once per
  * schedule and replayed as one CUDA graph (not while profiling, for the
- * two-sided layout or FedAdam; environment GCP_GRAPHS=0 disables it); results
+ * NCCL send/recv two-sided path or FedAdam; environment GCP_GRAPHS=0 disables it); results
  * are the same either way.  All three block; collective for nranks > 1. */
 gcp_status gcp_fit_begin(gcp_ctx* ctx, const gcp_fit_params* p, double* initial_est);
 gcp_status gcp_fit_epoch(gcp_ctx* ctx, double* est_out, int* accepted_out, int* done_out);

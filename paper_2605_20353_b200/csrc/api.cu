@@ -692,7 +692,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     if (use_fused) ST_TRY(fused_alloc(c, bytes));
     c->tsn_peer = false;
     if (use_fused && two_sided(c)) {
-        if (tsn_peer_wanted()) ST_TRY(tsn_peer_setup(c));   // K2 reaches the owners' rows directly
+        if (tsn_peer_wanted(c)) ST_TRY(tsn_peer_setup(c));   // K2 reaches the owners' rows directly
         else ST_TRY(tsn_alloc_bitmap(c));
     }
     {

@@ -350,7 +350,7 @@ gcp_status tsn_import(gcp_ctx* c, const SampleArgs& sa);
 gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower);
 gcp_status tsn_peer_setup(gcp_ctx* c);                          // the LSA base table (after fused_alloc)
 gcp_status tsn_peer_step(gcp_ctx* c, const gcp_adam_params* p, double lower);   // barrier + Adam + barrier
-bool tsn_peer_wanted();                                         // GCP_TWOSIDED_NVL=peer
+bool tsn_peer_wanted(const gcp_ctx* c);                         // peer access (default up to 8 ranks)
 
 }  // namespace gcp
 

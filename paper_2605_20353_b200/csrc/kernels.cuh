@@ -259,13 +259,16 @@ __global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(cons
                                 cv[e] = z;
                             }
                             if (dup) {   // rare: sum the other groups' vectors of the same row
+                                T own[VE];   // shuffled from an unmodified copy (every lane accumulates into cv)
+#pragma unroll
+                                for (int e = 0; e < VE; ++e) own[e] = cv[e];
 #pragma unroll
                                 for (int j = 1; j < SPR; ++j) {
                                     const int srcl = (lane + j * GL) & 31;
                                     const uint32_t ok2 = __shfl_sync(0xffffffffu, key, srcl);
                                     T o[VE];
 #pragma unroll
-                                    for (int e = 0; e < VE; ++e) o[e] = __shfl_sync(0xffffffffu, cv[e], srcl);
+                                    for (int e = 0; e < VE; ++e) o[e] = __shfl_sync(0xffffffffu, own[e], srcl);
                                     if (ok2 == key)
 #pragma unroll
                                         for (int e = 0; e < VE; ++e) cv[e] += o[e];

@@ -316,16 +316,24 @@ gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower) {
 
 namespace gcp {
 
-// ---- two-sided by peer access (GCP_TWOSIDED_NVL=peer) ---------------------
+// ---- two-sided by peer access (default; GCP_TWOSIDED_NVL=peer) ------------
 // K2 itself reaches every row owned elsewhere: it gathers the row from the
 // owner's A window and scatter-adds its contribution into the owner's G
 // window (red.global.add over NVLink), so only the touched rows cross the link
 // -- the paper's import and export, fused into the sampling kernel -- and no
 // touch pass, bitmap or copy is needed.  The step kernel then has every owner
 // update its rows between two LSA barriers.
-bool tsn_peer_wanted() {
+// The default two-sided implementation (up to 8 ranks): in the regime where
+// the two-sided layout beats the all-reduce at all -- few samples per
+// iteration against the replicated rows -- peer access is the faster one (c4
+// at 4 GPUs, 1e6 samples: 47.6 ms per epoch against 98.6 for the
+// import/export kernels and 95.3 for the fused all-reduce; at 1e7 / 1e8 the
+// all-reduce wins over both, profiles/r02m_*).  GCP_TWOSIDED_NVL=1 selects the
+// import / export kernels, =0 the NCCL send/recv path (twosided.cu).
+bool tsn_peer_wanted(const gcp_ctx* c) {
     const char* env = getenv("GCP_TWOSIDED_NVL");
-    return env && std::string(env) == "peer";
+    if (env) return std::string(env) == "peer";
+    return c->P <= 8;
 }
 
 __global__ void k_tsn_bases(ncclDevComm comm, ncclWindow_t winA, ncclWindow_t winG0, ncclWindow_t winG1, int P,
@@ -349,8 +357,9 @@ gcp_status tsn_peer_setup(gcp_ctx* c) {
 }
 
 // barrier (every member's K2 -- and so every red.add into my G rows -- is
-// complete); Alg. 1 on my owned rows of the current G; the other G parity
-// cleared (no member adds into it before the next barrier); barrier (every
+// complete); Alg. 1 on my owned rows of the current G, and the same rows of the
+// other G parity cleared in the same pass (no member adds into it before the
+// next barrier; rows owned elsewhere are never written here); barrier (every
 // owner's rows are updated before any next K2 gathers them)
 template <typename T>
 __global__ void __launch_bounds__(512) k_tsn_peer_step(ncclDevComm comm, T* __restrict__ A, const T* __restrict__ G,
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(512) k_tsn_peer_step(ncclDevComm comm, T* __re
     T* zp = reinterpret_cast<T*>(&z);
 #pragma unroll
     for (int q = 0; q < VE; ++q) zp[q] = T(0);
-    for (int64_t x = tid; x < n_coef / VE; x += nt) reinterpret_cast<V*>(Gnext)[x] = z;
+    (void)n_coef;
     for (int k = 0; k < ta.d; ++k) {
         const int64_t e0 = ta.off[k] + (int64_t)ta.me[k] * ta.shard[k] * ta.R_pad;
         const int64_t nv = ta.shard[k] * ta.R_pad / VE;
@@ -398,6 +407,9 @@ __global__ void __launch_bounds__(512) k_tsn_peer_step(ncclDevComm comm, T* __re
             *reinterpret_cast<V*>(A + e) = a;
             *reinterpret_cast<V*>(B + e) = bb;
             *reinterpret_cast<V*>(C + e) = cc;
+            // the other parity's G: only owned rows ever receive red.adds
+            // (every member adds into the owner's window), so only they are cleared
+            *reinterpret_cast<V*>(Gnext + e) = z;
         }
     }
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);

@@ -33,6 +33,8 @@ def main():
     if mode == "twosided_nccl":
         os.environ["GCP_TWOSIDED_NVL"] = "0"   # the NCCL send/recv two-sided path (twosided.cu)
         mode = "twosided"
+    if mode == "twosided":
+        os.environ["GCP_TWOSIDED_NVL"] = "1"   # the import / export kernels over NVLink windows (twosided_nvl.cu)
     peer = mode == "twosided_peer"
     if peer:
         os.environ["GCP_TWOSIDED_NVL"] = "peer"   # K2 reaches the owners' rows over NVLink (twosided_nvl.cu)
