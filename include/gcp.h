@@ -241,7 +241,10 @@ gcp_status gcp_sample_export(gcp_ctx* ctx, int stratum, int64_t first, int64_t c
 gcp_status gcp_loss_grad(gcp_ctx* ctx, gcp_loss loss, double* sampled_loss_out);
 
 /* Read G^(k)'s block rows ((hi_k-lo_k) x R doubles).  With nranks > 1 in sync
- * mode this is the LOCAL (pre-exchange) gradient.  Blocks. */
+ * mode this is the LOCAL (pre-exchange) gradient.  In the two-sided layout with
+ * peer access every rank adds into the owner's rows, so the rows this rank owns
+ * hold the slice group's summed gradient once every member's gcp_loss_grad has
+ * completed (the caller's barrier); other rows read as zero.  Blocks. */
 gcp_status gcp_grad_get(gcp_ctx* ctx, int k, double* out);
 
 /* ---- Adam (rows a6-a8; Alg. 1, Alg. 2-3) -------------------------- */

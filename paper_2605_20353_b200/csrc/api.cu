@@ -316,6 +316,7 @@ gcp_status checkpoint_restore(gcp_ctx* c) {
     if (!c->ag_interleaved) CUDA_TRY(c, cudaMemsetAsync(c->d_G, 0, bytes, c->stream), "restore");
     if (c->fused) CUDA_TRY(c, cudaMemsetAsync(c->d_G2, 0, bytes, c->stream), "restore");
     if (c->d_bm) CUDA_TRY(c, cudaMemsetAsync(c->d_bm, 0, tsn_bitmap_bytes(c), c->stream), "restore");
+    c->tsn_dirty = true;
     c->t = c->t_ck;
     c->ts = c->ts_ck;
     return GCP_OK;
@@ -752,6 +753,7 @@ gcp_status gcp_model_init(gcp_ctx* c, int R, uint64_t seed) {
     ST_TRY(ensure_partials(c, c->grad_blocks));
     c->have_model = true;
     c->have_grad = false;
+    c->tsn_dirty = true;      // peer access: a barrier before any member reads these rows
     return server_reset(c);   // FedAdam: U <- M0 (Alg. 4)
 }
 
@@ -780,6 +782,7 @@ gcp_status gcp_model_set(gcp_ctx* c, int k, const double* rows, const double* la
                  "model_set lambda");
         CUDA_TRY(c, cudaStreamSynchronize(c->stream), "model_set");
     }
+    c->tsn_dirty = true;
     return server_reset(c);   // FedAdam: the server copy starts from the model as set
 }
 
@@ -893,6 +896,7 @@ gcp_status gcp_loss_grad(gcp_ctx* c, gcp_loss loss, double* sampled_loss_out) {
     const SampleArgs s = sample_args(c, c->p_w, c->q_w, c->seed, c->it, KIND_GRAD_NZ, KIND_GRAD_Z, stratified);
     // two-sided layout (row f3): touch pass + import of the rows owned elsewhere
     if (two_sided(c) && !c->have_grad && !c->tsn_peer) ST_TRY(c->fused ? tsn_import(c, s) : twosided_import(c, s));
+    ST_TRY(tsn_peer_sync(c));
     const ModelArgs m = model_args(c);
     const int with_loss = sampled_loss_out != nullptr;
     cudaEvent_t ev;
@@ -1049,6 +1053,7 @@ gcp_status gcp_loss_estimate(gcp_ctx* c, gcp_loss loss, int64_t f_nz, int64_t f_
     double* dout = (double*)c->d_partials + c->partials_cap;
     // f-samples read any block row: refresh them (peer access reads the owners' rows)
     if (two_sided(c) && !c->tsn_peer) ST_TRY(dist_sync_exchange_post(c));
+    ST_TRY(tsn_peer_sync(c));
     ST_TRY(run_loss_kernel(c, loss, p, q, seed, 0xFFFFFFFFu, KIND_F_NZ, KIND_F_Z, 1, 0, PROF_LOSS, 1, dout));
     if (c->P > 1) ST_TRY(dist_allreduce_scalar(c, dout));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_scalar, dout, 8, cudaMemcpyDeviceToHost, c->stream), "loss_estimate");
@@ -1112,6 +1117,7 @@ static gcp_status epoch_graph(gcp_ctx* c, gcp_loss loss, const gcp_adam_params& 
                            (double)loss, (double)c->fused};
     const uint32_t it0 = c->it;
     const int64_t t0 = c->t;
+    ST_TRY(tsn_peer_sync(c));   // outside the graph: owed after a restore
     if (!c->graph_exec || memcmp(key, c->graph_key, sizeof(key)) != 0) {
         graph_drop(c);
         // a schedule seen once runs eagerly (a one-epoch job would pay the

@@ -169,6 +169,7 @@ struct gcp_ctx {
     void* d_bm = nullptr;                         // two-sided over NVLink: touched-row bits (2 parities)
     ncclWindow_t winBM = nullptr;
     bool tsn_peer = false;                        // two-sided over NVLink by peer access (no import / export)
+    bool tsn_dirty = false;                       // peer access: local A / G written outside the step kernel (barrier owed)
     void** d_peer_bases = nullptr;                // [3][8]: LSA bases of A, G, G2 of every rank
     // windows of the previous model kept registered for the next one of the same
     // size (a replace-ingest job skips the collective deregister / register)
@@ -351,6 +352,7 @@ gcp_status tsn_export(gcp_ctx* c, const gcp_adam_params* p, double lower);
 gcp_status tsn_peer_setup(gcp_ctx* c);                          // the LSA base table (after fused_alloc)
 gcp_status tsn_peer_step(gcp_ctx* c, const gcp_adam_params* p, double lower);   // barrier + Adam + barrier
 bool tsn_peer_wanted(const gcp_ctx* c);                         // peer access (default up to 8 ranks)
+gcp_status tsn_peer_sync(gcp_ctx* c);                           // LSA barrier if tsn_dirty (before peers read / add)
 
 }  // namespace gcp
 

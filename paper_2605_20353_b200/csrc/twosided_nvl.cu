@@ -353,6 +353,26 @@ gcp_status tsn_peer_setup(gcp_ctx* c) {
     TSN_CUDA(c, cudaGetLastError(), "peer bases");
     c->launches++;
     c->tsn_peer = true;
+    c->tsn_dirty = true;
+    return GCP_OK;
+}
+
+// Peer access makes every member's K2 read the owners' A rows and add into
+// their G rows, so a rank's own writes outside the step kernel (model init /
+// set, checkpoint restore: A and G rewritten on its stream) must be complete
+// on every rank before any member's next K2 -- one LSA barrier, owed from the
+// write to the next gradient or loss-estimate launch.
+__global__ void k_tsn_barrier(ncclDevComm comm) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamLsa(comm), comm.lsaBarrier, blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+gcp_status tsn_peer_sync(gcp_ctx* c) {
+    if (!c->tsn_peer || !c->tsn_dirty) return GCP_OK;
+    k_tsn_barrier<<<1, 128, 0, c->stream>>>(c->devcomm);
+    TSN_CUDA(c, cudaGetLastError(), "two-sided peer barrier");
+    c->launches++;
+    c->tsn_dirty = false;
     return GCP_OK;
 }
 

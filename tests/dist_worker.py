@@ -100,6 +100,9 @@ def main():
             if peer:
                 # peer access: every contribution to a row lands in its owner's G,
                 # so a rank holds the global (all-rank) gradient of its owned rows
+                # -- once every rank's gradient kernel has finished
+                torch.cuda.synchronize()
+                dist.barrier()
                 Gs, Ss, _ = oracle.sync_gradient(blocks, A_rank, loss, seed, it, p, q)
             for k in range(3):
                 Gg = ctx.grad_get(k)
@@ -173,4 +176,13 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    except BaseException:
+        # exit at once: a peer blocked in a device-side barrier would otherwise
+        # keep this rank's teardown (and the launcher) waiting; torchrun then
+        # stops the other ranks
+        import traceback
+        traceback.print_exc()
+        sys.stderr.flush()
+        os._exit(1)

@@ -1,6 +1,8 @@
 """Multi-GPU parity (needs >= 2 GPUs; run with `gpurun --gpus 2`): the sync
 (reduce-scatter / sharded Adam / all-gather), LocalSGD and FedAdam schemes,
 through the C ABI with NCCL, against the fp64 oracle's P-rank simulation."""
+import os
+import signal
 import subprocess
 import sys
 from pathlib import Path
@@ -24,9 +26,18 @@ def test_multi_gpu_parity(mode, nproc):
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            f"--nproc-per-node={nproc}", str(ROOT / "tests" / "dist_worker.py"), mode]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    errs = [ln for ln in (r.stdout + r.stderr).splitlines()
+    # own process group: on a timeout the launcher AND its workers are killed
+    # (a worker left spinning in a device-side barrier would hold its GPU)
+    pr = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT,
+                          start_new_session=True)
+    try:
+        out, err = pr.communicate(timeout=600)
+    except subprocess.TimeoutExpired:
+        os.killpg(pr.pid, signal.SIGKILL)
+        out, err = pr.communicate()
+        pytest.fail(f"{mode} at {nproc} GPUs timed out\n" + err[-1500:])
+    errs = [ln for ln in (out + err).splitlines()
             if "Error" in ln or "assert" in ln or "GCP_E" in ln][:20]
-    assert r.returncode == 0, "\n".join(errs) + "\n" + r.stderr[-1500:]
-    assert "DIST-OK" in r.stdout
-    print([ln for ln in r.stdout.splitlines() if "DIST-OK" in ln][0])
+    assert pr.returncode == 0, "\n".join(errs) + "\n" + err[-1500:]
+    assert "DIST-OK" in out
+    print([ln for ln in out.splitlines() if "DIST-OK" in ln][0])
