@@ -42,9 +42,17 @@ constexpr int kRejectCap = 1000;      // reading R5
 #ifndef GCP_RBREG
 #define GCP_RBREG 8
 #endif
+#ifndef GCP_SMALL_MINB
+#define GCP_SMALL_MINB 3
+#endif
+#ifndef GCP_SMALL_RBREG
+#define GCP_SMALL_RBREG 8
+#endif
 constexpr int kBlock = GCP_BLOCK;          // threads per CTA of the sample kernels
 constexpr int kSampleMinBlocks = GCP_MINB; // resident CTAs per SM the register budget must allow
 constexpr int kRowRegBudget = GCP_RBREG;   // 16-B row vectors per lane kept in flight per batch
+constexpr int kSmallMinBlocks = GCP_SMALL_MINB;   // the same two for small row footprints (D * NV <= 3)
+constexpr int kSmallRowRegBudget = GCP_SMALL_RBREG;
 constexpr double kHashLoad = 0.5;     // target hash-set load factor
 
 enum Kind : uint32_t { KIND_GRAD_NZ = 0, KIND_GRAD_Z = 1, KIND_F_NZ = 2, KIND_F_Z = 3, KIND_INIT = 4 };

@@ -90,14 +90,20 @@ __device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, 
 // processes the 32 samples in GL rounds of 32/GL samples, a sample per group of
 // GL lanes, each lane owning NV 16-byte vectors of every factor row.  Rounds are
 // handled RB at a time with all their row loads issued before any arithmetic.
-// Register budget per instantiation: small row footprints (D*NV <= 3) run at
-// 4 CTAs/SM (64 regs) with one row batch in flight; larger ones at
-// kSampleMinBlocks with kRowRegBudget row vectors in flight (B200 K2 tuning,
-// profiles/r01_summary.md).
-template <int D, int NV> struct SampleGeom {
+// Register budget per instantiation: small fp32 row footprints (D*NV <= 3:
+// c2, c4, c5) run at kSmallMinBlocks = 3 CTAs/SM (80 regs) with two rounds of
+// row loads in flight -- more loads in flight per warp beat a fourth CTA when
+// rows come from DRAM (c4 K2 2.61 -> 2.48 ms, c2 1.205 -> 1.192 ms against 4
+// CTAs x one round; 2 CTAs x 2 or 4 rounds were slower, profiles/r02q_*);
+// small fp64 footprints (the parity mode) 3 CTAs/SM with one round (their
+// doubles need the registers); larger ones run at kSampleMinBlocks with kRowRegBudget row
+// vectors in flight (B200 K2 tuning, profiles/r01_summary.md).
+template <typename T, int D, int NV> struct SampleGeom {
     static constexpr bool small = D * NV <= 3;
-    static constexpr int minb = small ? 4 : kSampleMinBlocks;
-    static constexpr int rowregs = small ? 4 : kRowRegBudget;
+    static constexpr bool f32 = sizeof(T) == 4;
+    static constexpr int minb = small ? (f32 ? kSmallMinBlocks : 3) : kSampleMinBlocks;
+    static constexpr int rowregs = small ? (f32 ? kSmallRowRegBudget : 4) : kRowRegBudget;
+    static constexpr int rbcap = small ? 2 : 4;   // rounds per load batch at most
 };
 
 // position s of the visiting order -> slot (identity unless a slot order is given)
@@ -115,14 +121,14 @@ __device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t s, int64
 enum { kVarPlain = 0, kVarPeer = 1, kVarWagg = 2 };
 
 template <typename T, int D, int GL, int NV, int VAR = kVarPlain>
-__global__ void __launch_bounds__(kBlock, SampleGeom<D, NV>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
+__global__ void __launch_bounds__(kBlock, SampleGeom<T, D, NV>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
                                                    const KParams<T> kp) {
     constexpr int VE = Vec16<T>::n;
     constexpr int SPR = 32 / GL;                 // samples per round
     // rounds per load batch: bounded so the row registers (RB*D*NV*16 B) fit the
     // budget (a power of two, so it divides GL)
-    constexpr int RB_REG = SampleGeom<D, NV>::rowregs / (D * NV);
-    constexpr int RB_CAP = GL < 4 ? GL : 4;
+    constexpr int RB_REG = SampleGeom<T, D, NV>::rowregs / (D * NV);
+    constexpr int RB_CAP = GL < SampleGeom<T, D, NV>::rbcap ? GL : SampleGeom<T, D, NV>::rbcap;
     constexpr int RB = RB_REG >= 4 && RB_CAP >= 4 ? 4 : (RB_REG >= 2 && RB_CAP >= 2 ? 2 : 1);
     const int lane = threadIdx.x & 31;
     const int grp = lane / GL, gl = lane % GL;
