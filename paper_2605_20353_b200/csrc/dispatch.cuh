@@ -14,10 +14,10 @@ static cudaError_t run_sample(gcp_ctx* c, const SampleArgs& s, const ModelArgs& 
     return cudaGetLastError();
 }
 
-template <typename T, int D, int GL, int NV>
+template <typename T, int D, int GL, int NV, int VAR = kVarPlain>
 static int occ_sample() {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sample<T, D, GL, NV>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sample<T, D, GL, NV, VAR>, kBlock, 0);
     return nb;
 }
 
@@ -50,8 +50,9 @@ struct SampleLaunch {
         return run_sample<T, D, GL, NV, VAR>(c, *s, *m, *static_cast<const KParams<T>*>(kp), nblocks);
     }
 };
+template <int VAR = kVarPlain>
 struct SampleOcc {
-    template <typename T, int D, int GL, int NV> int operator()() const { return occ_sample<T, D, GL, NV>(); }
+    template <typename T, int D, int GL, int NV> int operator()() const { return occ_sample<T, D, GL, NV, VAR>(); }
 };
 
 // one K2 launch of variant VAR (kernels_f32.cu / kernels_f64.cu instantiate the
@@ -69,9 +70,9 @@ cudaError_t sample_kernel_T(gcp_ctx* c, const SampleArgs& s, const ModelArgs& m,
     return mode_switch<T>(c->d, nvec, SampleLaunch<VAR>{c, &s, &m, &kp, nblocks});
 }
 
-template <typename T>
+template <typename T, int VAR = kVarPlain>
 int sample_occupancy_T(int d, int R_pad) {
-    return mode_switch<T>(d, R_pad / Vec16<T>::n, SampleOcc{});
+    return mode_switch<T>(d, R_pad / Vec16<T>::n, SampleOcc<VAR>{});
 }
 
 template <typename T>

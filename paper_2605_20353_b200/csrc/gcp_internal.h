@@ -48,6 +48,12 @@ constexpr int kRejectCap = 1000;      // reading R5
 #ifndef GCP_SMALL_RBREG
 #define GCP_SMALL_RBREG 8
 #endif
+#ifndef GCP_PEER_MINB
+#define GCP_PEER_MINB 0   // > 0: the peer-access K2's own CTAs/SM and row budget (GCP_PEER_RBREG)
+#endif
+#ifndef GCP_PEER_RBREG
+#define GCP_PEER_RBREG 8
+#endif
 constexpr int kBlock = GCP_BLOCK;          // threads per CTA of the sample kernels
 constexpr int kSampleMinBlocks = GCP_MINB; // resident CTAs per SM the register budget must allow
 constexpr int kRowRegBudget = GCP_RBREG;   // 16-B row vectors per lane kept in flight per batch

@@ -23,6 +23,8 @@ cudaError_t sample_kernel_wagg_f64(gcp_ctx*, const SampleArgs&, const ModelArgs&
                               int, double*, int, const OrdHistArgs*);
 int sample_occupancy_f32(int, int);
 int sample_occupancy_f64(int, int);
+int sample_occupancy_peer_f32(int, int);
+int sample_occupancy_peer_f64(int, int);
 cudaError_t export_f32(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
                        int32_t*);
 cudaError_t export_f64(gcp_ctx*, const SampleArgs&, int64_t, int64_t, const int64_t*, int64_t*, int64_t*,
@@ -35,7 +37,10 @@ cudaError_t init_f32(gcp_ctx*, const InitArgs&, void*);
 cudaError_t init_f64(gcp_ctx*, const InitArgs&, void*);
 
 int sample_kernel_blocks(gcp_ctx* c) {
-    const int occ = c->prec == GCP_FP32 ? sample_occupancy_f32(c->d, c->R_pad) : sample_occupancy_f64(c->d, c->R_pad);
+    // persistent grid: the resident CTAs of the variant the context launches
+    const bool f32 = c->prec == GCP_FP32;
+    const int occ = c->tsn_peer ? (f32 ? sample_occupancy_peer_f32(c->d, c->R_pad) : sample_occupancy_peer_f64(c->d, c->R_pad))
+                                : (f32 ? sample_occupancy_f32(c->d, c->R_pad) : sample_occupancy_f64(c->d, c->R_pad));
     return c->sm_count * (occ > 0 ? occ : 1);
 }
 

@@ -98,12 +98,14 @@ __device__ __forceinline__ void ord_hist_slot(const OrdHistArgs& oh, int64_t s, 
 // small fp64 footprints (the parity mode) 3 CTAs/SM with one round (their
 // doubles need the registers); larger ones run at kSampleMinBlocks with kRowRegBudget row
 // vectors in flight (B200 K2 tuning, profiles/r01_summary.md).
-template <typename T, int D, int NV> struct SampleGeom {
+template <typename T, int D, int NV, int VAR = 0> struct SampleGeom {
     static constexpr bool small = D * NV <= 3;
     static constexpr bool f32 = sizeof(T) == 4;
-    static constexpr int minb = small ? (f32 ? kSmallMinBlocks : 3) : kSampleMinBlocks;
-    static constexpr int rowregs = small ? (f32 ? kSmallRowRegBudget : 4) : kRowRegBudget;
-    static constexpr int rbcap = small ? 2 : 4;   // rounds per load batch at most
+    // the peer-access variant's remote rows (NVLink latency) may want more in flight
+    static constexpr bool peer = VAR == 1 && GCP_PEER_MINB > 0;
+    static constexpr int minb = peer ? GCP_PEER_MINB : small ? (f32 ? kSmallMinBlocks : 3) : kSampleMinBlocks;
+    static constexpr int rowregs = peer ? GCP_PEER_RBREG : small ? (f32 ? kSmallRowRegBudget : 4) : kRowRegBudget;
+    static constexpr int rbcap = peer ? 4 : small ? 2 : 4;   // rounds per load batch at most
 };
 
 // position s of the visiting order -> slot (identity unless a slot order is given)
@@ -121,14 +123,14 @@ __device__ __forceinline__ int64_t slot_at(const SampleArgs& a, int64_t s, int64
 enum { kVarPlain = 0, kVarPeer = 1, kVarWagg = 2 };
 
 template <typename T, int D, int GL, int NV, int VAR = kVarPlain>
-__global__ void __launch_bounds__(kBlock, SampleGeom<T, D, NV>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
+__global__ void __launch_bounds__(kBlock, SampleGeom<T, D, NV, VAR>::minb) k_sample(const SampleArgs sa, const ModelArgs ma,
                                                    const KParams<T> kp) {
     constexpr int VE = Vec16<T>::n;
     constexpr int SPR = 32 / GL;                 // samples per round
     // rounds per load batch: bounded so the row registers (RB*D*NV*16 B) fit the
     // budget (a power of two, so it divides GL)
-    constexpr int RB_REG = SampleGeom<T, D, NV>::rowregs / (D * NV);
-    constexpr int RB_CAP = GL < SampleGeom<T, D, NV>::rbcap ? GL : SampleGeom<T, D, NV>::rbcap;
+    constexpr int RB_REG = SampleGeom<T, D, NV, VAR>::rowregs / (D * NV);
+    constexpr int RB_CAP = GL < SampleGeom<T, D, NV, VAR>::rbcap ? GL : SampleGeom<T, D, NV, VAR>::rbcap;
     constexpr int RB = RB_REG >= 4 && RB_CAP >= 4 ? 4 : (RB_REG >= 2 && RB_CAP >= 2 ? 2 : 1);
     const int lane = threadIdx.x & 31;
     const int grp = lane / GL, gl = lane % GL;

@@ -9,4 +9,5 @@ cudaError_t sample_kernel_peer_f64(gcp_ctx* c, const SampleArgs& s, const ModelA
                                   const OrdHistArgs* oh) {
     return sample_kernel_T<double, kVarPeer>(c, s, m, loss, loss_mode, semi_nz, w_nz, w_z, with_loss, partials, nb, oh);
 }
+int sample_occupancy_peer_f64(int d, int R_pad) { return sample_occupancy_T<double, kVarPeer>(d, R_pad); }
 }  // namespace gcp
