@@ -167,6 +167,25 @@ def main():
     for k in range(3):
         want = (Af if omode == "sync" else Af[rank])[k][mine.lo[k]:mine.hi[k]]
         assert np.allclose(ctx.model_get(k), want, rtol=TM_FIT, atol=TM), f"replace-ingest fit model k={k}"
+    if omode == "sync":
+        # a rejected epoch (R20): at rate 0.3 the oracle accepts, rejects (restore
+        # of A, B, C, t; rate x 0.1), then accepts twice -- the restore rewrites
+        # every rank's rows, which the next gradient (peer access: remote reads
+        # and adds) must only see after all ranks restored
+        ctx.model_init(R, 77)
+        kw3 = dict(kw, rate=0.3, epochs=4)
+        fp3 = ctx.fit_params(iters_per_epoch=6, loss=loss, tau=0, meta_rate=5e-3, **kw3)
+        _, rows3 = ctx.fit(fp3)
+        Af3, hist3, _ = oracle.fit(blocks, grid, A0, loss, iters=6, mode="sync", tau=tau, meta_rate=5e-3, **kw3)
+        assert [h[2] for h in hist3] == [True, False, True, True], hist3
+        assert len(rows3) == len(hist3), (rows3, hist3)
+        for r, h in zip(rows3, hist3):
+            # the trace reports the rate after the epoch's decision (x decay on a rejection)
+            r_after = h[1] * (1.0 if h[2] else kw3["decay"])
+            assert abs(r[2] - h[0]) <= TE_FIT * abs(h[0]) and abs(r[3] - r_after) <= 1e-12 * r_after, ("rejection", r, h)
+        for k in range(3):
+            assert np.allclose(ctx.model_get(k), Af3[k][mine.lo[k]:mine.hi[k]], rtol=TM_FIT, atol=TM), \
+                f"rejection fit model k={k}"
     ctx.close()
     dist.barrier()
     if rank == 0:

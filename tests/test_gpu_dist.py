@@ -39,5 +39,8 @@ def test_multi_gpu_parity(mode, nproc):
     errs = [ln for ln in (out + err).splitlines()
             if "Error" in ln or "assert" in ln or "GCP_E" in ln][:20]
     assert pr.returncode == 0, "\n".join(errs) + "\n" + err[-1500:]
+    # the bounds-checked build (GCP_LIB=libgcp_bounds.so) prints device-side violations
+    bounds = [ln for ln in (out + err).splitlines() if "GCP-BOUNDS" in ln]
+    assert not bounds, "\n".join(bounds[:10])
     assert "DIST-OK" in out
     print([ln for ln in out.splitlines() if "DIST-OK" in ln][0])
