@@ -84,7 +84,8 @@ typedef enum {
     GCP_DIST_ASYNC_AVG = 1,       /* LocalSGD averaging every tau iterations (Alg. 3) */
     GCP_DIST_ASYNC_FEDADAM = 2,   /* FedAdam server step every tau iterations (Alg. 4) */
     GCP_DIST_SYNC_TWO_SIDED = 3   /* "two-sided" layout: rows partitioned, per-iteration import/export;
-                                     gcp_model_get and gcp_loss_estimate are collective in this mode.  Within one
+                                     gcp_model_get, gcp_model_set and gcp_loss_estimate are collective in this
+                                     mode (every rank calls them in the same order).  Within one
                                      NVLink domain of <= 8 ranks the gradient kernel reaches the owners' rows by
                                      peer access (environment GCP_TWOSIDED_NVL=1: import/export kernels over
                                      NVLink windows; =0: NCCL send/recv) */
