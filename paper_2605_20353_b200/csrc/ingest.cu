@@ -146,9 +146,13 @@ __global__ void k_filter_insert(int64_t n, const uint64_t* __restrict__ klo, con
 
 // Filter size: ~16 bits per key in a power-of-two number of 32-B sectors,
 // capped at min(64 MB, 0.55 L2) so it stays L2-resident next to the factors;
-// off below min_bits per key (4 in front of the sorted search, 12 in front of
-// the hash: c2 keeps the plain hash, c4/c5 have no filter at all).
-// GCP_FILTER=0 disables it, GCP_FILTER_MB sets the cap.
+// off below min_bits = 4 per key (c4 / c5 have no filter at all).  c2 gets 5.4
+// bits per key (~8% "maybe"): K2 1.204 -> 1.177 ms against the plain hash
+// probe under the final K2 geometry, and 1e7 fewer DRAM bucket reads per
+// launch keep the clocks off the power cap (profiles/r02aa_*; round 1, with one
+// round of row loads in flight, measured it the other way and kept it off).
+// GCP_FILTER=0 disables it, GCP_FILTER_MB sets the cap, GCP_FILTER_MINBITS the
+// threshold.
 static uint64_t filter_sectors_for(const gcp_ctx* c, int64_t nnz, int min_bits) {
     const char* env = getenv("GCP_FILTER");
     if ((env && std::string(env) == "0") || nnz <= 0) return 0;
@@ -158,6 +162,8 @@ static uint64_t filter_sectors_for(const gcp_ctx* c, int64_t nnz, int min_bits) 
     const uint64_t want = (uint64_t)nnz * 2;
     uint64_t bytes = 32;
     while (bytes < want && bytes * 2 <= cap) bytes <<= 1;
+    const char* mbits = getenv("GCP_FILTER_MINBITS");   // A/B switch for the bits-per-key threshold
+    if (mbits) min_bits = atoi(mbits);
     if (bytes * 8 < (uint64_t)nnz * min_bits) return 0;
     return bytes / 32;
 }
@@ -361,7 +367,7 @@ static gcp_status ingest_impl(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
     uint64_t* new_hash = nullptr;
     uint64_t* new_keys = nullptr;
     uint64_t* new_filter = nullptr;
-    const uint64_t fsect = filter_sectors_for(c, nnz, sorted_member ? 4 : 12);
+    const uint64_t fsect = filter_sectors_for(c, nnz, 4);
     // diagnostics: GCP_INGEST_TRACE=1 syncs after each phase and prints its time
     const char* trace_env = getenv("GCP_INGEST_TRACE");
     const bool trace = trace_env && trace_env[0] == '1';
@@ -547,7 +553,7 @@ static gcp_status ingest_lean(gcp_ctx* c, const gcp_ctx* g, int64_t nnz, const i
     uint64_t* new_keys = nullptr;
     uint64_t* new_filter = nullptr;
     uint64_t slots = 4;
-    const uint64_t fsect = filter_sectors_for(c, nnz, sorted_member ? 4 : 12);
+    const uint64_t fsect = filter_sectors_for(c, nnz, 4);
 
     CK(smalloc(c, &d_flags, sizeof(unsigned)));
     CK(cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st));
