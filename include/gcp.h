@@ -4,7 +4,7 @@
  * is cited as P:line with the section / equation / algorithm named).
  *
  * One gcp_ctx per rank == per GPU.  Implemented by libgcp.so
- * (paper_2605_20353_b200/csrc/*.cu, sm_100a only).  No torch types cross this
+ * (the .cu sources under paper_2605_20353_b200/csrc/, sm_100a only).  No torch types cross this
  * boundary: host pointers are plain C arrays, the CUDA stream is an opaque
  * cudaStream_t, the NCCL unique id is 128 opaque bytes.
  *
