@@ -604,10 +604,19 @@ def roofline(w, name, alg_bytes, p_loc, k2_ms, peak, peak_src, layout):
         return dict(base, bound="hbm", peak=peak, frac=achieved / peak, peak_source=peak_src)
     m = json.loads((ROOT / "profiles" / "membench_r01.json").read_text())
     if w["d"] == 3 and w["R"] * 4 == 64 and "k2_skeleton_dram_ms_per_2e7" in m:
-        sk_ms = m["k2_skeleton_dram_ms_per_2e7"] * 2 * p_loc / 2e7
+        # skeleton = L2 gathers + red.add rows, plus one random DRAM read for the
+        # samples that make one: every nonzero (its record); a zero candidate only
+        # on an L2 Bloom filter "maybe" (~8% at c2's 5.4 bits per key) when the
+        # filter is in front of the hash, else every zero (its bucket)
+        fz = 0.08 if (layout or {}).get("filter") else 1.0
+        frac_dram = (1.0 + fz) / 2.0   # p = q
+        per2e7 = m["k2_skeleton_l2_ms_per_2e7"] + (m["k2_skeleton_dram_ms_per_2e7"] - m["k2_skeleton_l2_ms_per_2e7"]) * frac_dram
+        sk_ms = per2e7 * 2 * p_loc / 2e7
         return dict(base, bound="l2", peak=alg_bytes / (sk_ms * 1e-3) / 1e9, frac=sk_ms / k2_ms,
                     peak_source=("measured K2 memory skeleton on this pool (profiles/membench_r01.json "
-                                 "k2_skeleton_dram_ms_per_2e7, tools/membench.cu): " f"{sk_ms:.3f} ms per launch"),
+                                 "k2_skeleton_l2_ms_per_2e7 + the random DRAM read of "
+                                 f"{frac_dram:.2f} of the samples from k2_skeleton_dram_ms_per_2e7, tools/membench.cu): "
+                                 f"{sk_ms:.3f} ms per launch"),
                     hbm_view={"peak": peak, "frac": achieved / peak, "peak_source": peak_src,
                               "note": "algorithmic bytes over HBM copy bandwidth: > 1 because the factor rows "
                                       "and G hit in L2; dram.frac_of_hbm is the DRAM view"})
