@@ -40,7 +40,7 @@ constexpr int kRejectCap = 1000;      // reading R5
 #define GCP_MINB 2
 #endif
 #ifndef GCP_RBREG
-#define GCP_RBREG 8
+#define GCP_RBREG 10
 #endif
 #ifndef GCP_SMALL_MINB
 #define GCP_SMALL_MINB 3
